@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""bench.py -- FMM target evaluations per second on B200 (BASELINE.json metric).
+
+A step = one pass of the whole hot path (fmm_build_tree + fmm_evaluate: keying,
+radix sort, lists, P2M, M2M, M2L/L2L, L2P+P2P) over each tiling of the workload.
+Default workload: config C4 of BASELINE.json (the 16.8M-point tiling comparison:
+quadtree L9, septree L6, triangle-quadtree L9, N = M = 16,777,216 self-mode
+points, p = 24, seed 3) -- the configuration the metric is quoted on.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C3|C5|C1|C2]
+  python bench.py --impl reference ...     (the CPU oracle, bounded sample)
+
+Multi-GPU (torchrun, one process per GPU): every rank gets the full input
+(replicated), builds the tree and the upward pass redundantly and evaluates its
+own range of target leaves (no data-path collective: DESIGN.md "Multi-GPU");
+time = max over ranks; value = all targets / time (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fmm_inputs as fi  # noqa: E402
+
+METRIC = "FMM target evals/sec (FP64, 16M pts) at 1/2/4/8 B200; P2P/M2L % FP64 peak"
+WORKLOADS = {
+    "C4": ["C4q", "C4s", "C4t"],
+    "C3": ["C3"],
+    "C5": ["C5"],
+    "C1": ["C1"],
+    "C2": ["C2"],
+    "C4q": ["C4q"],
+    "C4s": ["C4s"],
+    "C4t": ["C4t"],
+}
+# FP64 peak derived from the unit counts and clocks of the guides:
+# 148 SMs x 64 FP64 FMA/clk/SM x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# FP64 flops per P2P pair executed by the P2P kernel (ncu-measured)
+F_PAIR = float(os.environ.get("FMM_F_PAIR", "0")) or None
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self):
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def stop(self, dev_index=0):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.samples if len(r) >= 8 and r[0] == str(dev_index)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- inputs
+def make_inputs(names):
+    out = {}
+    for nm in names:
+        w = fi.get(nm)
+        t0 = time.time()
+        out[nm] = (w, fi.generate(w))
+        log(f"[bench] generated {nm} ({w.note}) in {time.time() - t0:.1f}s")
+    return out
+
+
+def counters_for(tree):
+    from paper_1204_3105_b200 import X
+
+    return tree.export(X.COUNTERS)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_3105_b200 as fmm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    names = WORKLOADS[args.workload]
+    inputs = make_inputs(names)
+    stream = torch.cuda.current_stream(dev)
+
+    def cfg_of(w):
+        return fmm.Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, w.self_mode,
+                               rank=rank, nranks=world)
+
+    # device-resident inputs and outputs
+    dev_in, host_in, outs, host_out = {}, {}, {}, {}
+    for nm, (w, d) in inputs.items():
+        dev_in[nm] = (torch.from_numpy(d["src_xy"]).to(dev), torch.from_numpy(d["u"]).to(dev),
+                      None if d["tgt_xy"] is None else torch.from_numpy(d["tgt_xy"]).to(dev))
+        host_in[nm] = tuple(None if a is None else torch.from_numpy(a).pin_memory()
+                            for a in (d["src_xy"], d["u"], d["tgt_xy"]))
+        outs[nm] = torch.zeros(w.m, dtype=torch.complex128, device=dev)
+        host_out[nm] = torch.zeros(w.m, dtype=torch.complex128).pin_memory()
+
+    def one_step(timing=False, host=False):
+        launches, stage = 0, {}
+        for nm, (w, d) in inputs.items():
+            src, u, tgt = host_in[nm] if host else dev_in[nm]
+            t = fmm.Tree(cfg_of(w), src, u, tgt, stream=stream)
+            if timing:
+                t.set_timing(True)
+            t.evaluate(host_out[nm] if host else outs[nm], stream=stream)
+            launches += t.launch_count()
+            if timing:
+                stage[nm] = t
+            else:
+                t.close()
+        return launches, stage
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up (also checks device status once)
+    for i in range(args.warmup):
+        one_step()
+    barrier()
+    # correctness guard: status of one tree
+    for nm, (w, d) in inputs.items():
+        src, u, tgt = dev_in[nm]
+        t = fmm.Tree(cfg_of(w), src, u, tgt, stream=stream)
+        t.evaluate(outs[nm], stream=stream)
+        t.check()
+        cnt = counters_for(t)
+        inputs[nm] = (w, d, cnt)
+        t.close()
+    inputs2 = {nm: v[:2] for nm, v in inputs.items()}
+    counters = {nm: v[2] for nm, v in inputs.items()}
+    inputs.clear()
+    inputs.update(inputs2)
+
+    # ---- timed region: device-resident inputs
+    clocks = Clocks()
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    p2p_ms, down_ms, up_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
+    for s in range(args.steps):
+        n_l, trees = one_step(timing=True)
+        launches += n_l
+        for nm, t in trees.items():
+            ms = t.stage_times()
+            up_ms[nm] += ms[3]
+            down_ms[nm] += ms[4]
+            p2p_ms[nm] += ms[5]
+            t.close()
+    e1.record(stream)
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    clk = clocks.stop(local)
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_targets = sum(inputs[nm][0].m for nm in names) * args.steps
+
+    # ---- e2e: same metric through the C ABI with pinned host buffers (H2D + D2H inside)
+    for i in range(1):
+        one_step(host=True)
+    barrier()
+    t0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for s in range(args.steps):
+        one_step(host=True)
+    f1.record(stream)
+    barrier()
+    e2e_ms = f0.elapsed_time(f1)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_t.item())
+    h2d = sum(w.n * 24 + (0 if w.self_mode else w.m * 16) for w, _ in inputs.values())
+    d2h = sum(w.m * 16 for w, _ in inputs.values())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    # ---- roofline of the dominant kernel (P2P + fused L2P), measured with CUDA events
+    pairs = {nm: int(counters[nm][1]) for nm in names}
+    p2p_ms_avg = sum(p2p_ms.values()) / args.steps  # per step, all tilings
+    pair_rate = sum(pairs.values()) / (p2p_ms_avg / 1e3) if p2p_ms_avg > 0 else 0.0
+    f_pair = F_PAIR
+    roof = {"kernel": "k_p2p (P2P near field + fused L2P)", "bound": "alu", "unit": "TFLOP/s",
+            "peak": round(FP64_PEAK_TFLOPS, 2),
+            "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md Roofline); "
+                           "DFMA microbenchmark 34.2 TF/s (profiles/)",
+            "pairs_per_s": pair_rate, "f_pair_flops": f_pair, "traffic": None}
+    if f_pair:
+        ach = pair_rate * f_pair / 1e12
+        roof.update({"achieved": round(ach, 3), "frac": round(ach / FP64_PEAK_TFLOPS, 4)})
+    else:
+        roof.update({"achieved": None, "frac": None})
+
+    per_tiling = {nm: {"p2p_ms": p2p_ms[nm] / args.steps, "downward_ms": down_ms[nm] / args.steps,
+                       "upward_ms": up_ms[nm] / args.steps, "p2p_pairs": pairs[nm],
+                       "m2l_ops": int(counters[nm][0])} for nm in names}
+    value = total_targets / (ms_max / 1e3)
+    res = {
+        "metric": METRIC, "value": value, "unit": "target evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded numpy PCG64 (fmm_inputs), shapes of BASELINE.json configs",
+        "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
+                   "tilings": names, "step": "fmm_build_tree + fmm_evaluate per tiling",
+                   "l2": "inputs larger than L2 (>= 400 MB per tiling)", "per_tiling": per_tiling},
+        "roofline": roof,
+        "e2e": {"value": total_targets / (e2e_ms / 1e3), "unit": "target evals/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        res["cpu_baseline"] = cpu_baseline(args, names, sample_targets=args.cpu_sample)
+    if world > 1:
+        dist.destroy_process_group()
+    return res
+
+
+# ---------------------------------------------------------------- oracle (CPU) arm
+def oracle_time(w, d, sample_targets, seed=0):
+    """Oracle as it stands on a bounded sample of the workload: full keying, sort and
+    upward pass over all points, downward + L2P + P2P for `sample_targets` random
+    targets; extrapolated to all M targets (per-target work is independent)."""
+    import oracle
+
+    cfg = oracle.config(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, w.self_mode)
+    t0 = time.perf_counter()
+    T = oracle.Tree(cfg, d["src_xy"], d["u"], d["tgt_xy"])
+    T.upward()
+    t1 = time.perf_counter()
+    rng = np.random.default_rng(seed)
+    ids = np.sort(rng.choice(w.m, size=min(sample_targets, w.m), replace=False))
+    T.evaluate(ids)
+    t2 = time.perf_counter()
+    est = (t1 - t0) + (t2 - t1) * (w.m / len(ids))
+    return est, t2 - t0, len(ids)
+
+
+def cpu_baseline(args, names, sample_targets):
+    import oracle
+
+    inputs = {nm: (fi.get(nm), fi.generate(fi.get(nm))) for nm in names}
+    est, spent, ns = 0.0, 0.0, 0
+    for nm, (w, d) in inputs.items():
+        e, s, k = oracle_time(w, d, sample_targets)
+        est += e
+        spent += s
+        ns += k
+    total = sum(w.m for w, _ in inputs.values())
+    return {"value": total / est, "unit": "target evals/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"full keying+sort+upward pass on every point of {', '.join(names)}, downward+L2P+P2P "
+                      f"for {sample_targets} random targets per tiling, extrapolated to all targets; "
+                      f"{spent:.1f} s of CPU wall time"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+
+    names = WORKLOADS[args.workload]
+    inputs = {nm: (fi.get(nm), fi.generate(fi.get(nm))) for nm in names}
+    # each step: a bounded sample of the workload (see oracle_time)
+    for i in range(args.warmup):
+        pass  # the oracle has no warm state worth discarding; warm-up steps are skipped
+    ests, spent = [], 0.0
+    for s in range(args.steps):
+        est = 0.0
+        for nm, (w, d) in inputs.items():
+            e, sp, _ = oracle_time(w, d, args.cpu_sample, seed=s)
+            est += e
+            spent += sp
+        ests.append(est)
+    total = sum(w.m for w, _ in inputs.values())
+    ms = 1e3 * sum(ests) / len(ests)
+    value = total / (ms / 1e3)
+    cores = oracle.num_threads()
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "target evals/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, seeded numpy PCG64 (fmm_inputs)",
+            "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
+                       "tilings": names},
+            "cpu_baseline": {"value": value, "unit": "target evals/s", "cores": cores, "kind": "oracle",
+                             "sample": f"per step: full keying+sort+upward pass, {args.cpu_sample} sampled targets "
+                                       f"per tiling, extrapolated; {spent:.1f} s CPU wall time total"},
+            "e2e": {"value": value, "unit": "target evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    args = ap.parse_args()
+    res = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

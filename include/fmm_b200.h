@@ -1,0 +1,161 @@
+/*
+ * fmm_b200.h -- C ABI of the B200-native FMM hot path (libfmm_b200.so).
+ *
+ * Computes, for the complex log kernel of arXiv:1204.3105 section 2,
+ *     Phi_j = sum_i u_i * Log(y_j - x_i),   j = 1..M           (eqs. 1-2)
+ * by the hierarchical FMM on a fixed-depth square quadtree, septree (hexagons,
+ * GBT addressing, section 5) or triangle-quadtree (section 6), with the
+ * interaction lists of section 4 (Neighbors / NeighborsE4, read as a
+ * set difference: DESIGN.md D1) and the classical 2D log-kernel operators the
+ * paper cites but omits (D10).  Every step runs in this
+ * library's own sm_100a CUDA kernels, in FP64.
+ *
+ * Plain C99: no C++ or torch types.  All functions are thread-compatible (one
+ * tree per thread at a time).  Streams are passed as `void*` holding a
+ * cudaStream_t (NULL = legacy default stream).
+ *
+ * Error codes (return values):
+ *   FMM_OK            0
+ *   FMM_EBADCFG       1  invalid configuration / argument
+ *   FMM_EDOMAIN       2  a point lies outside the root domain (index: fmm_last_error_index)
+ *   FMM_ECOINCIDENT   3  a target coincides with a source of another index (D16)
+ *   FMM_ECUDA         4  CUDA runtime error (message: fmm_error_string / fmm_last_error_message)
+ *   FMM_ENOMEM        5  device allocation failed
+ *   FMM_EEXTENSION    7  the library was built without support for the request
+ * Domain and coincidence errors are detected on the device; they are reported
+ * by the next synchronising call (fmm_status, fmm_export).
+ */
+#ifndef FMM_B200_H
+#define FMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMM_OK 0
+#define FMM_EBADCFG 1
+#define FMM_EDOMAIN 2
+#define FMM_ECOINCIDENT 3
+#define FMM_ECUDA 4
+#define FMM_ENOMEM 5
+#define FMM_EEXTENSION 7
+
+/* tilings: square quadtree (Morton Z), septree, triangle-quadtree */
+#define FMM_QUADTREE 0
+#define FMM_SEPTREE 1
+#define FMM_TRIQUAD 2
+
+/* Configuration.  Frames (D7, D8, D11):
+ *   FMM_QUADTREE: root_x, root_y = lower-left corner of the root square; root_size = its side.
+ *   FMM_SEPTREE : root_x, root_y = centre of leaf cell 0 (origin of the leaf lattice);
+ *                 root_size = R0, circumradius of the idealised root hexagon; the leaf
+ *                 circumradius is r = R0 / (7^floor(L/2) * (L odd ? sqrt(7) : 1)); the domain
+ *                 is the island of the 7^L leaf hexagons (reading D8).
+ *   FMM_TRIQUAD : root_x, root_y = centroid of the upright root triangle; root_size = its
+ *                 circumradius R0 (level-l circumradius R0 * 2^-l).
+ * depth  L: quadtree / triangle 1..15, septree 1..10 (leaf keys must fit 32 bits).
+ * p       : expansion terms, 1..31 (multipole Q, a_1..a_p; local b_0..b_p).
+ * self_mode: 1 when targets are the sources; the pair (i, i) is skipped by index (D16).
+ * rank / nranks: target-leaf partition for multi-GPU runs;
+ *                single GPU: 0 / 1.  Rank r evaluates the targets of leaf range
+ *                [K*r/nranks, K*(r+1)/nranks) of its work-balanced split; see fmm_rank_range. */
+typedef struct {
+  int32_t tiling;
+  int32_t depth;
+  int32_t p;
+  int32_t self_mode;
+  double root_x;
+  double root_y;
+  double root_size;
+  int32_t rank;
+  int32_t nranks;
+  int32_t reserved[6]; /* must be zero */
+} fmm_config;
+
+typedef struct fmm_tree_s* fmm_tree_t;
+
+/* Build the tree: leaf keys (CellIndex, P:207-250 / P:342-364 / Morton), a stable
+ * radix sort of points by (leaf key, input index), leaf CSR offsets, cell centres
+ * (CellCenter, bit-exact lattice form D12) and the near / E4 interaction lists.
+ *
+ * src_xy: n points as interleaved (x, y) float64 pairs (complex128 layout);
+ * src_u : n real float64 strengths; tgt_xy: m points (ignored, may be NULL, in
+ * self_mode where m must equal n).  Pointers may be device memory (used in
+ * place) or host memory (copied to the device on `stream`; pinned memory makes
+ * the copies asynchronous).  The library copies what it needs: inputs may be
+ * freed or overwritten once the work on `stream` completes.
+ * n == 0 or m == 0 is valid (potentials are then zero / empty).
+ * On success *out owns all device buffers until fmm_free. */
+int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* src_u, int64_t n,
+                   const double* tgt_xy, int64_t m, void* stream, fmm_tree_t* out);
+
+/* Evaluate Phi for all m targets of this rank: P2M, M2M (upward), M2L + L2L per
+ * level (downward), then L2P fused with the P2P near field.  phi_out: m complex128
+ * values (interleaved re, im) in the caller's target order; device or host memory
+ * (host: copied back on `stream`; the caller synchronises the stream).  Targets
+ * owned by other ranks are left untouched. */
+int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream);
+
+/* Replace the strengths (same geometry) so the tree can be re-evaluated. */
+int fmm_set_strengths(fmm_tree_t t, const double* src_u, void* stream);
+
+/* Synchronise the tree's stream and return the first device-detected error. */
+int fmm_status(fmm_tree_t t);
+/* offending input index of the last FMM_EDOMAIN (source index, or n + target index)
+ * / FMM_ECOINCIDENT (target index); -1 if none */
+int64_t fmm_last_error_index(fmm_tree_t t);
+
+/* Exports for parity tests (synchronising, host buffers).  Returns the byte count
+ * needed in *needed; copies min(bytes, needed) into host_buf when non-NULL.
+ *   FMM_X_SRC_KEYS / FMM_X_TGT_KEYS : uint32 per input point (leaf index, input order)
+ *   FMM_X_SRC_PERM / FMM_X_TGT_PERM : int32 per sorted position -> input index
+ *   FMM_X_SRC_OFFSETS / FMM_X_TGT_OFFSETS : int64 [K+1] leaf CSR over the sorted order
+ *   FMM_X_CENTRES  (level)  : float64 (x, y) per cell of the level, all B^level cells
+ *   FMM_X_NEAR_OWNERS / _OFFSETS / _ENTRIES : near lists (D17) of the non-empty
+ *                     target leaves: int32 owners ascending, int64 offsets, int32 entries
+ *   FMM_X_E4_OWNERS / _OFFSETS / _ENTRIES (level) : NeighborsE4 lists likewise
+ *   FMM_X_MULTIPOLE (level) : complex128 [B^level][p+1] (Q, a_1..a_p), after fmm_evaluate
+ *   FMM_X_LOCAL     (level) : complex128 [B^level][p+1] (b_0..b_p) of evaluated cells
+ *   FMM_X_COUNTERS : int64 [4] = {M2L ops, P2P pairs, non-empty source leaves, non-empty target leaves} */
+#define FMM_X_SRC_KEYS 1
+#define FMM_X_TGT_KEYS 2
+#define FMM_X_SRC_PERM 3
+#define FMM_X_TGT_PERM 4
+#define FMM_X_SRC_OFFSETS 5
+#define FMM_X_TGT_OFFSETS 6
+#define FMM_X_CENTRES 7
+#define FMM_X_NEAR_OWNERS 8
+#define FMM_X_NEAR_OFFSETS 9
+#define FMM_X_NEAR_ENTRIES 10
+#define FMM_X_E4_OWNERS 11
+#define FMM_X_E4_OFFSETS 12
+#define FMM_X_E4_ENTRIES 13
+#define FMM_X_MULTIPOLE 14
+#define FMM_X_LOCAL 15
+#define FMM_X_COUNTERS 16
+int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t bytes, size_t* needed);
+
+/* Per-stage device times (ms) of the last build / evaluate when timing is enabled
+ * with fmm_set_timing(t, 1): {keys, sort, lists, p2m+m2m, downward, p2p}. */
+int fmm_set_timing(fmm_tree_t t, int32_t enable);
+int fmm_stage_times(fmm_tree_t t, float* ms6);
+
+/* Leaf range [lo, hi) of target leaves evaluated by cfg->rank (balanced by the
+ * estimated near-field work; requires a built tree for the counts). */
+int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi);
+
+/* Number of this library's kernel launches enqueued by the last build / evaluate. */
+int64_t fmm_launch_count(fmm_tree_t t);
+
+void fmm_free(fmm_tree_t t);
+const char* fmm_error_string(int code);
+const char* fmm_last_error_message(void);
+int fmm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -82,8 +82,12 @@ def lib():
             "orc_tree_count": (C.c_int64, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32]),
             "orc_tree_near": (C.c_int, [C.c_void_p, C.c_int64, _i64]),
             "orc_tree_e4": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, _i64]),
+            "orc_tree_near_csr": (C.c_int, [C.c_void_p, _i32, _i64, _i32, _i64, _i64]),
+            "orc_tree_e4_csr": (C.c_int, [C.c_void_p, C.c_int32, _i32, _i64, _i32, _i64, _i64]),
+            "orc_tree_centres": (None, [C.c_void_p, C.c_int32, _d]),
             "orc_tree_upward": (None, [C.c_void_p]),
             "orc_tree_multipole": (None, [C.c_void_p, C.c_int32, C.c_int64, _d]),
+            "orc_tree_multipoles_level": (None, [C.c_void_p, C.c_int32, _d]),
             "orc_tree_local": (None, [C.c_void_p, C.c_int32, C.c_int64, _d]),
             "orc_tree_evaluate": (C.c_int, [C.c_void_p, _i64, C.c_int64, _d, _i64, _i64]),
             "orc_tree_bound": (None, [C.c_void_p, _i64, C.c_int64, _d]),
@@ -335,6 +339,33 @@ class Tree:
         k = lib().orc_tree_e4(self.h, level, cell, _ptr(out, _i64))
         return out[:k].copy()
 
+    def _csr(self, level):
+        no, ne = C.c_int64(), C.c_int64()
+        if level is None:
+            lib().orc_tree_near_csr(self.h, None, None, None, C.byref(no), C.byref(ne))
+        else:
+            lib().orc_tree_e4_csr(self.h, level, None, None, None, C.byref(no), C.byref(ne))
+        ow = np.zeros(no.value, np.int32)
+        of = np.zeros(no.value + 1, np.int64)
+        en = np.zeros(ne.value, np.int32)
+        if level is None:
+            lib().orc_tree_near_csr(self.h, _ptr(ow, _i32), _ptr(of, _i64), _ptr(en, _i32), C.byref(no), C.byref(ne))
+        else:
+            lib().orc_tree_e4_csr(self.h, level, _ptr(ow, _i32), _ptr(of, _i64), _ptr(en, _i32), C.byref(no),
+                                  C.byref(ne))
+        return ow, of, en
+
+    def near_csr(self):
+        return self._csr(None)
+
+    def e4_csr(self, level):
+        return self._csr(level)
+
+    def centres(self, level):
+        xy = np.zeros((self.B ** level, 2))
+        lib().orc_tree_centres(self.h, level, _ptr(xy, _d))
+        return xy
+
     def upward(self):
         lib().orc_tree_upward(self.h)
 
@@ -342,6 +373,11 @@ class Tree:
         self.upward()
         mp = np.zeros(self.p + 1, np.complex128)
         lib().orc_tree_multipole(self.h, level, cell, mp.ctypes.data_as(_d))
+        return mp
+
+    def multipoles(self, level):
+        mp = np.zeros((self.B ** level, self.p + 1), np.complex128)
+        lib().orc_tree_multipoles_level(self.h, level, mp.ctypes.data_as(_d))
         return mp
 
     def local(self, level, cell):

@@ -935,6 +935,44 @@ int orc_tree_e4(const orc_tree* t, int32_t l, int64_t cell, int64_t* out) {
   return q;
 }
 
+/* canonical CSR of near (level < 0) or E4 (level l) lists over non-empty target cells */
+static int lists_csr(const orc_tree* t, int l, int32_t* owners, int64_t* offs, int32_t* entries, int64_t* nown,
+                     int64_t* nent) {
+  int level = l < 0 ? t->L : l;
+  int64_t nc = ipow(t->B, level), no = 0, ne = 0;
+  int64_t buf[128];
+  if (offs) offs[0] = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    if (t->tcnt[level][c] == 0) continue;
+    int k = l < 0 ? orc_tree_near(t, c, buf) : orc_tree_e4(t, level, c, buf);
+    if (owners) owners[no] = (int32_t)c;
+    for (int a = 0; a < k; ++a) {
+      if (entries) entries[ne] = (int32_t)buf[a];
+      ++ne;
+    }
+    ++no;
+    if (offs) offs[no] = ne;
+  }
+  *nown = no;
+  *nent = ne;
+  return ORC_OK;
+}
+int orc_tree_near_csr(const orc_tree* t, int32_t* owners, int64_t* offs, int32_t* entries, int64_t* nown,
+                      int64_t* nent) {
+  return lists_csr(t, -1, owners, offs, entries, nown, nent);
+}
+int orc_tree_e4_csr(const orc_tree* t, int32_t level, int32_t* owners, int64_t* offs, int32_t* entries,
+                    int64_t* nown, int64_t* nent) {
+  if (level < 1 || level > t->L) return ORC_EBADCFG;
+  return lists_csr(t, level, owners, offs, entries, nown, nent);
+}
+
+static const double* centre_of(orc_tree* t, int l, int64_t cell);
+void orc_tree_centres(orc_tree* t, int32_t level, double* xy) {
+  const double* c = centre_of(t, level, 0);
+  memcpy(xy, c, 16 * (size_t)ipow(t->B, level));
+}
+
 static const double* centre_of(orc_tree* t, int l, int64_t cell) {
   if (!t->cen[l]) {
 #pragma omp critical
@@ -978,6 +1016,11 @@ void orc_tree_upward(orc_tree* t) {
     }
   }
   t->upward_done = 1;
+}
+
+void orc_tree_multipoles_level(orc_tree* t, int32_t l, double* mp) {
+  orc_tree_upward(t);
+  memcpy(mp, t->mp[l], sizeof(cplx) * (size_t)(t->p + 1) * (size_t)ipow(t->B, l));
 }
 
 void orc_tree_multipole(const orc_tree* t, int32_t l, int64_t cell, double* mp) {

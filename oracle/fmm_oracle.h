@@ -99,9 +99,19 @@ int64_t orc_tree_count(const orc_tree* t, int32_t level, int64_t cell, int32_t w
 /* interaction lists restricted to non-empty source cells, ascending (D17) */
 int orc_tree_near(const orc_tree* t, int64_t leaf, int64_t* out);
 int orc_tree_e4(const orc_tree* t, int32_t level, int64_t cell, int64_t* out);
+/* the same lists as canonical CSR over the non-empty target cells (ascending):
+ * owners [nown], offsets [nown+1], entries [nent].  Call with NULL buffers to get the
+ * sizes in *nown / *nent. */
+int orc_tree_near_csr(const orc_tree* t, int32_t* owners, int64_t* offs, int32_t* entries, int64_t* nown,
+                      int64_t* nent);
+int orc_tree_e4_csr(const orc_tree* t, int32_t level, int32_t* owners, int64_t* offs, int32_t* entries,
+                    int64_t* nown, int64_t* nent);
+/* CellCenter of every cell of a level (exact-lattice form, D12) */
+void orc_tree_centres(orc_tree* t, int32_t level, double* xy);
 /* upward pass over all cells (P2M + M2M) -- must be called before the getters below */
 void orc_tree_upward(orc_tree* t);
 void orc_tree_multipole(const orc_tree* t, int32_t level, int64_t cell, double* mp);
+void orc_tree_multipoles_level(orc_tree* t, int32_t level, double* mp); /* all cells of a level */
 /* local expansion of a target cell (computed on demand, level-ordered recursion) */
 void orc_tree_local(orc_tree* t, int32_t level, int64_t cell, double* loc);
 /* Phi at targets tgt_ids (original indices; NULL = all), returns ORC_ECOINCIDENT + *bad */

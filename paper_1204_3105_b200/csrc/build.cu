@@ -1,0 +1,468 @@
+// build.cu -- tree build on the device: keying (CellIndex), stable LSD radix sort by
+// (leaf key, input index), leaf CSR offsets, cell centres and interaction lists.
+//   keying      : PAPER.md P:207-250 (septree), P:342-364 (triangle), P:79 (Morton)
+//   sort / CSR  : "Indexing: cell indices satisfy some order relation in memory"
+//   lists       : P:101-111 Neighbors / NeighborsE4 (set-difference reading D1, from level 1: D2)
+#include <limits.h>
+
+#include "fmm_internal.cuh"
+#include "geometry.cuh"
+
+namespace {
+
+DGeo dgeo(const Geo& g) {
+  DGeo d;
+  d.tiling = g.tiling;
+  d.L = g.L;
+  d.B = g.B;
+  d.K = g.K;
+  d.root_x = g.root_x;
+  d.root_y = g.root_y;
+  d.root_size = g.root_size;
+  d.sept_A = g.sept_A;
+  d.sept_Bc = g.sept_Bc;
+  d.sept_D3r = g.sept_D3r;
+  return d;
+}
+
+// ------------------------------------------------------------------ keying
+// key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
+// and report the minimal offending index; histogram of keys (K+1 bins) for the CSR.
+__global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
+                                              int64_t index_base, uint32_t* __restrict__ key,
+                                              int32_t* __restrict__ hist, DevStatus* st) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 p = xy[i];
+  uint32_t k;
+  if (!geo_key(g, p.x, p.y, &k)) {
+    k = (uint32_t)g.K;
+    atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
+  }
+  key[i] = k;
+  // warp-aggregated histogram increment
+  unsigned peers = __match_any_sync(__activemask(), k);
+  int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[k], __popc(peers));
+}
+
+// ------------------------------------------------------------------ scan (exclusive, int32)
+constexpr int SCAN_T = 1024, SCAN_I = 8, SCAN_TILE = SCAN_T * SCAN_I;
+
+__device__ inline int block_excl_scan(int v, int* total) {
+  __shared__ int warp_tot[32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;  // inclusive
+  }
+  __syncthreads();
+  int before = w ? warp_tot[w - 1] : 0;
+  *total = warp_tot[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const int32_t* __restrict__ in, int64_t n,
+                                                         int32_t* __restrict__ bsum) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_I; ++k)
+    if (base + k < n) s += in[base + k];
+  int tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_block_sums(int32_t* bsum, int64_t nb) {
+  // single block, exclusive scan of up to SCAN_TILE block sums, in place
+  int64_t base = threadIdx.x * SCAN_I;
+  int v[SCAN_I], s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_I; ++k) {
+    v[k] = base + k < nb ? bsum[base + k] : 0;
+    s += v[k];
+  }
+  int tot;
+  int run = block_excl_scan(s, &tot);
+#pragma unroll
+  for (int k = 0; k < SCAN_I; ++k) {
+    if (base + k < nb) bsum[base + k] = run;
+    run += v[k];
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_apply(const int32_t* in, int64_t n, const int32_t* __restrict__ bsum,
+                                                        int32_t* out) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
+  int v[SCAN_I], s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_I; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    s += v[k];
+  }
+  int tot;
+  int run = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < SCAN_I; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+}
+
+// ------------------------------------------------------------------ LSD radix sort (8-bit digits)
+constexpr int RS_T = 256, RS_ROUNDS = 16, RS_TILE = RS_T * RS_ROUNDS;
+
+__global__ void __launch_bounds__(RS_T) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                                          int32_t* __restrict__ tile_hist, int ntiles) {
+  __shared__ int cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * RS_TILE;
+  for (int r = 0; r < RS_ROUNDS; ++r) {
+    int64_t i = base + r * RS_T + threadIdx.x;
+    if (i < n) {
+      unsigned d = (keys[i] >> shift) & 255u;
+      unsigned peers = __match_any_sync(__activemask(), d);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// stable scatter: element order within a tile = (round, warp, lane); ranks from warp
+// match masks plus a per-digit prefix over warps and rounds.
+__global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __restrict__ keys,
+                                                            const int32_t* __restrict__ vals, int64_t n, int shift,
+                                                            const int32_t* __restrict__ tile_off, int ntiles,
+                                                            uint32_t* __restrict__ keys_out,
+                                                            int32_t* __restrict__ vals_out) {
+  __shared__ int gofs[256];
+  __shared__ int base[256];
+  __shared__ int wcnt[RS_T / 32][256];
+  __shared__ int wpre[RS_T / 32][256];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  gofs[t] = tile_off[(int64_t)t * ntiles + blockIdx.x];
+  base[t] = 0;
+#pragma unroll
+  for (int q = 0; q < RS_T / 32; ++q) wcnt[q][t] = 0;
+  __syncthreads();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int64_t tile0 = (int64_t)blockIdx.x * RS_TILE;
+  for (int r = 0; r < RS_ROUNDS; ++r) {
+    int64_t i = tile0 + r * RS_T + t;
+    bool valid = i < n;
+    uint32_t k = valid ? keys[i] : 0u;
+    int32_t v = valid ? (vals ? vals[i] : (int32_t)i) : 0;
+    unsigned d = valid ? ((k >> shift) & 255u) : (256u + lane);
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    int rank = __popc(peers & lt_mask);
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][d] = __popc(peers);
+    __syncthreads();
+    {
+      int run = base[t];
+#pragma unroll
+      for (int q = 0; q < RS_T / 32; ++q) {
+        int c = wcnt[q][t];
+        wpre[q][t] = run;
+        wcnt[q][t] = 0;
+        run += c;
+      }
+      base[t] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      int pos = gofs[d] + wpre[w][d] + rank;
+      keys_out[pos] = k;
+      vals_out[pos] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gathers
+__global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
+                             const double* __restrict__ u, double2* __restrict__ sxy, double* __restrict__ su) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t j = perm[i];
+  sxy[i] = xy[j];
+  su[i] = u[j];
+}
+__global__ void k_gather_xy(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
+                            double2* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = xy[perm[i]];
+}
+
+// ------------------------------------------------------------------ centres (D12)
+__global__ void k_centres(DGeo g, int l, int64_t ncells, double2* __restrict__ out) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  out[c] = geo_centre(g, l, c);
+}
+
+// ------------------------------------------------------------------ interaction lists
+__device__ inline int32_t cell_count(const int32_t* __restrict__ off, int64_t cell, int64_t span) {
+  return off[(cell + 1) * span] - off[cell * span];
+}
+
+__device__ inline void sort_small(int64_t* v, int n) {
+  for (int i = 1; i < n; ++i) {
+    int64_t x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+}
+
+// One thread per parent P at level l-1.  Candidates = Children(P U Neighbors(P, l-1))
+// with sources, ascending; for every child t with targets, e4mask bit i is set iff
+// cand[i] is not in {t} U Neighbors(t, l)  (NeighborsE4, reading D1).
+__global__ void k_lists_level(DGeo g, int l, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                              int32_t* __restrict__ cand, int32_t* __restrict__ ncand,
+                              unsigned long long* __restrict__ e4mask, int64_t leaf_lo, int64_t leaf_hi) {
+  int64_t P = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t nparents = ipow_d(g.B, l - 1);
+  if (P >= nparents) return;
+  const int B = g.B;
+  int64_t span_l = ipow_d(B, g.L - l), span_p = span_l * B;
+  // parent's target range intersected with this rank's leaf range
+  int64_t lo = P * span_p, hi = lo + span_p;
+  bool has_t = (hi > leaf_lo && lo < leaf_hi) &&
+               (toff[min(hi, leaf_hi)] - toff[max(lo, leaf_lo)] > 0);
+  int32_t* my = cand + P * FMM_CAND_MAX;
+  unsigned long long* masks = e4mask;  // level-local
+  if (!has_t) {
+    ncand[P] = 0;
+    for (int ch = 0; ch < B; ++ch) masks[P * B + ch] = 0ull;
+    return;
+  }
+  int64_t pn[16];
+  int npn = geo_neighbors(g, l - 1, P, pn);
+  int64_t c[FMM_CAND_MAX];
+  int nc = 0;
+  for (int q = -1; q < npn; ++q) {
+    int64_t Q = q < 0 ? P : pn[q];
+    for (int ch = 0; ch < B; ++ch) {
+      int64_t cc = Q * B + ch;
+      if (cell_count(soff, cc, span_l) > 0) c[nc++] = cc;
+    }
+  }
+  sort_small(c, nc);
+  for (int i = 0; i < nc; ++i) my[i] = (int32_t)c[i];
+  ncand[P] = nc;
+  for (int ch = 0; ch < B; ++ch) {
+    int64_t t = P * B + ch;
+    int64_t tl = t * span_l, th = tl + span_l;
+    bool t_has = (th > leaf_lo && tl < leaf_hi) && (toff[min(th, leaf_hi)] - toff[max(tl, leaf_lo)] > 0);
+    unsigned long long mask = 0ull;
+    if (t_has) {
+      int64_t nb[16];
+      int nn = geo_neighbors(g, l, t, nb);
+      for (int i = 0; i < nc; ++i) {
+        bool near = (c[i] == t);
+        for (int k = 0; k < nn; ++k) near |= (c[i] == nb[k]);
+        if (!near) mask |= 1ull << i;
+      }
+    }
+    masks[t] = mask;
+  }
+}
+
+// near(t) = ({t} U Neighbors(t, L)) with sources, ascending
+__global__ void k_near(DGeo g, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                       int32_t* __restrict__ near, int32_t* __restrict__ nnear, int64_t leaf_lo, int64_t leaf_hi) {
+  int64_t t = leaf_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= leaf_hi) return;
+  if (toff[t + 1] - toff[t] == 0) {
+    nnear[t] = 0;
+    return;
+  }
+  int64_t nb[17];
+  int nn = geo_neighbors(g, g.L, t, nb);
+  nb[nn++] = t;
+  int64_t v[17];
+  int k = 0;
+  for (int i = 0; i < nn; ++i)
+    if (soff[nb[i] + 1] - soff[nb[i]] > 0) v[k++] = nb[i];
+  sort_small(v, k);
+  for (int i = 0; i < k; ++i) near[t * FMM_NEAR_MAX + i] = (int32_t)v[i];
+  nnear[t] = k;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ====================================================================== host entry points
+size_t fmm_scan_scratch_bytes(int64_t n) {
+  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  return (size_t)(nb + 32) * sizeof(int32_t);
+}
+
+int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
+                        cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return FMM_OK;
+  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb > SCAN_TILE || scratch_bytes < fmm_scan_scratch_bytes(n)) return FMM_EBADCFG;
+  int32_t* bsum = (int32_t*)scratch;
+  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum);
+  k_scan_block_sums<<<1, SCAN_T, 0, s>>>(bsum, nb);
+  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum, out);
+  *launches += 3;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
+  int b = 1;
+  while (((int64_t)1 << b) <= K) ++b;
+  return b;
+}
+
+// sort (key, iota) pairs stably; writes the permutation (sorted position -> input index)
+static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm) {
+  if (n == 0) return FMM_OK;
+  cudaStream_t s = t->stream;
+  int bits = key_bits(t->g.K);
+  int passes = (bits + 7) / 8;
+  int ntiles = (int)((n + RS_TILE - 1) / RS_TILE);
+  int64_t nhist = (int64_t)256 * ntiles;
+  // scratch: kA kB (n u32), vA (n i32), hist (nhist), scan scratch
+  size_t need = (size_t)n * 4 * 3 + (size_t)nhist * 4 + fmm_scan_scratch_bytes(nhist) + 256;
+  if (t->scratch_bytes < need) {
+    if (t->scratch) cudaFreeAsync(t->scratch, s);
+    t->scratch = nullptr;
+    FMM_CUDA_TRY(cudaMallocAsync(&t->scratch, need, s));
+    t->scratch_bytes = need;
+  }
+  char* p = (char*)t->scratch;
+  uint32_t* kA = (uint32_t*)p;
+  p += (size_t)n * 4;
+  uint32_t* kB = (uint32_t*)p;
+  p += (size_t)n * 4;
+  int32_t* vA = (int32_t*)p;
+  p += (size_t)n * 4;
+  int32_t* hist = (int32_t*)p;
+  p += (size_t)nhist * 4;
+  void* sscr = p;
+  const uint32_t* kin = keys;
+  const int32_t* vin = nullptr;  // iota on the first pass
+  for (int ps = 0; ps < passes; ++ps) {
+    uint32_t* kout = (ps % 2 == 0) ? kA : kB;
+    // values alternate between vA and perm such that the last pass writes perm
+    int32_t* vout = ((passes - 1 - ps) % 2 == 0) ? perm : vA;
+    k_radix_upsweep<<<ntiles, RS_T, 0, s>>>(kin, n, 8 * ps, hist, ntiles);
+    int e = fmm_device_scan_i32(hist, hist, nhist, sscr, fmm_scan_scratch_bytes(nhist), s, &t->launches);
+    if (e) return e;
+    k_radix_downsweep<<<ntiles, RS_T, 0, s>>>(kin, vin, n, 8 * ps, hist, ntiles, kout, vout);
+    t->launches += 2;
+    FMM_CUDA_TRY(cudaGetLastError());
+    kin = kout;
+    vin = vout;
+  }
+  return FMM_OK;
+}
+
+int fmm_stage_keys_sort(fmm_tree_s* t) {
+  cudaStream_t s = t->stream;
+  const Geo& G = t->g;
+  DGeo g = dgeo(G);
+  int64_t K = G.K;
+  // histograms (K+1 bins incl. sentinel), zeroed
+  FMM_CUDA_TRY(cudaMemsetAsync(t->soff, 0, sizeof(int32_t) * (K + 2), s));
+  if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->toff, 0, sizeof(int32_t) * (K + 2), s));
+  if (t->n > 0) {
+    k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->soff,
+                                                  t->status);
+    t->launches++;
+  }
+  if (!G.self_mode && t->m > 0) {
+    k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->toff,
+                                                  t->status);
+    t->launches++;
+  }
+  FMM_CUDA_TRY(cudaGetLastError());
+  // exclusive scans of the histograms -> leaf CSR (soff[K] = #in-domain points)
+  size_t sb = fmm_scan_scratch_bytes(K + 2);
+  void* scr = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync(&scr, sb, s));
+  int e = fmm_device_scan_i32(t->soff, t->soff, K + 2, scr, sb, s, &t->launches);
+  if (!e && !G.self_mode) e = fmm_device_scan_i32(t->toff, t->toff, K + 2, scr, sb, s, &t->launches);
+  cudaFreeAsync(scr, s);
+  if (e) return e;
+  e = radix_sort_perm(t, t->skey, t->n, t->sperm);
+  if (!e && !G.self_mode) e = radix_sort_perm(t, t->tkey, t->m, t->tperm);
+  if (e) return e;
+  if (t->n > 0) {
+    k_gather_src<<<blocks_for(t->n, 256), 256, 0, s>>>(t->sperm, t->n, (const double2*)t->src_xy_in, t->src_u_in,
+                                                        t->sxy, t->su);
+    t->launches++;
+  }
+  if (!G.self_mode && t->m > 0) {
+    k_gather_xy<<<blocks_for(t->m, 256), 256, 0, s>>>(t->tperm, t->m, (const double2*)t->tgt_xy_in, t->txy);
+    t->launches++;
+  }
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+int fmm_stage_tables_lists(fmm_tree_s* t) {
+  cudaStream_t s = t->stream;
+  const Geo& G = t->g;
+  DGeo g = dgeo(G);
+  for (int l = 0; l <= G.L; ++l) {
+    k_centres<<<blocks_for(G.ncells[l], 256), 256, 0, s>>>(g, l, G.ncells[l], t->centre + G.lvl_off[l]);
+    t->launches++;
+  }
+  for (int l = 1; l <= G.L; ++l) {
+    int64_t np = G.ncells[l - 1];
+    k_lists_level<<<blocks_for(np, 128), 128, 0, s>>>(g, l, t->soff, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
+                                                      t->ncand + G.lvl_off[l - 1], t->e4mask + G.lvl_off[l],
+                                                      t->leaf_lo, t->leaf_hi);
+    t->launches++;
+  }
+  int64_t nl = t->leaf_hi - t->leaf_lo;
+  if (nl > 0) {
+    k_near<<<blocks_for(nl, 128), 128, 0, s>>>(g, t->soff, t->toff, t->near, t->nnear, t->leaf_lo, t->leaf_hi);
+    t->launches++;
+  }
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+namespace {
+__global__ void k_gather_u(const int32_t* __restrict__ perm, int64_t n, const double* __restrict__ u,
+                           double* __restrict__ su) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) su[i] = u[perm[i]];
+}
+}  // namespace
+
+int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u) {
+  if (t->n == 0) return FMM_OK;
+  k_gather_u<<<blocks_for(t->n, 256), 256, 0, t->stream>>>(t->sperm, t->n, u, t->su);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}

@@ -1,0 +1,473 @@
+// capi.cu -- the C ABI of include/fmm_b200.h: configuration checks, device memory
+// (one stream-ordered slab per tree), host<->device staging, stage sequencing, exports.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fmm_internal.cuh"
+
+static thread_local std::string g_last_msg;
+void fmm_set_error_message(const std::string& s) { g_last_msg = s; }
+
+namespace {
+
+constexpr int BS = 2 * FMM_MAX_P + 2;
+
+std::vector<double> host_binom() {
+  std::vector<double> b((size_t)BS * BS, 0.0);
+  for (int n = 0; n < BS; ++n) {
+    b[(size_t)n * BS] = 1.0;
+    for (int k = 1; k <= n; ++k) b[(size_t)n * BS + k] = b[(size_t)(n - 1) * BS + k - 1] + (k < n ? b[(size_t)(n - 1) * BS + k] : 0.0);
+  }
+  return b;
+}
+
+void init_pool_once() {
+  static std::once_flag f;
+  std::call_once(f, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int64_t ipow64(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+int make_geo(const fmm_config* c, Geo* g) {
+  if (!c) return FMM_EBADCFG;
+  if (c->tiling < 0 || c->tiling > 2) return FMM_EBADCFG;
+  if (c->p < 1 || c->p > FMM_MAX_P - 1) return FMM_EBADCFG;
+  if (c->depth < 1 || c->depth > (c->tiling == FMM_SEPTREE ? 10 : 15)) return FMM_EBADCFG;
+  if (!(c->root_size > 0.0) || !isfinite(c->root_x) || !isfinite(c->root_y)) return FMM_EBADCFG;
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return FMM_EBADCFG;
+  for (int i = 0; i < 6; ++i)
+    if (c->reserved[i]) return FMM_EBADCFG;
+  memset(g, 0, sizeof(*g));
+  g->tiling = c->tiling;
+  g->L = c->depth;
+  g->B = c->tiling == FMM_SEPTREE ? 7 : 4;
+  g->p = c->p;
+  g->self_mode = c->self_mode ? 1 : 0;
+  g->K = ipow64(g->B, g->L);
+  g->lvl_off[0] = 0;
+  for (int l = 0; l <= g->L; ++l) {
+    g->ncells[l] = ipow64(g->B, l);
+    g->lvl_off[l + 1] = g->lvl_off[l] + g->ncells[l];
+  }
+  g->total_cells = g->lvl_off[g->L + 1];
+  g->root_x = c->root_x;
+  g->root_y = c->root_y;
+  g->root_size = c->root_size;
+  if (g->tiling == FMM_SEPTREE) {
+    // leaf circumradius r = R0 / (7^floor(L/2) * (L odd ? sqrt 7 : 1))  (reading D8); fixed IEEE sequence
+    volatile double den = (double)ipow64(7, g->L / 2);
+    if (g->L % 2) den = den * sqrt(7.0);
+    volatile double r = c->root_size / den;
+    g->sept_r = r;
+    volatile double A = 1.5 * r;
+    volatile double s3r = 1.7320508075688772 * r;
+    volatile double Bc = 0.5 * s3r;
+    volatile double D3r = 3.0 * r;
+    g->sept_A = A;
+    g->sept_Bc = Bc;
+    g->sept_D3r = D3r;
+  }
+  return FMM_OK;
+}
+
+// bump allocator over one cudaMallocAsync slab
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
+    T* p = (T*)(base ? base + off : nullptr);
+    off += bytes;
+    return p;
+  }
+};
+
+void carve(fmm_tree_s* t, Arena& a) {
+  const Geo& G = t->g;
+  int64_t n = t->n, m = t->m, K = G.K;
+  int64_t inner = G.total_cells - G.ncells[G.L];
+  t->skey = a.take<uint32_t>(n + 1);
+  t->sperm = a.take<int32_t>(n + 1);
+  t->soff = a.take<int32_t>(K + 2);
+  t->sxy = a.take<double2>(n + 1);
+  t->su = a.take<double>(n + 1);
+  if (G.self_mode) {
+    t->tkey = t->skey;
+    t->tperm = t->sperm;
+    t->toff = t->soff;
+    t->txy = t->sxy;
+  } else {
+    t->tkey = a.take<uint32_t>(m + 1);
+    t->tperm = a.take<int32_t>(m + 1);
+    t->toff = a.take<int32_t>(K + 2);
+    t->txy = a.take<double2>(m + 1);
+  }
+  t->centre = a.take<double2>(G.total_cells);
+  t->cand = a.take<int32_t>(inner * FMM_CAND_MAX);
+  t->ncand = a.take<int32_t>(inner);
+  t->e4mask = a.take<unsigned long long>(G.total_cells);
+  t->near = a.take<int32_t>(K * FMM_NEAR_MAX);
+  t->nnear = a.take<int32_t>(K);
+  t->ntask_cap = m / 32 + (t->leaf_hi - t->leaf_lo) + 1;
+  t->task_leaf = a.take<int32_t>(t->ntask_cap);
+  t->task_start = a.take<int32_t>(t->ntask_cap);
+  t->ntask = a.take<int32_t>(1);
+  t->mp = a.take<double2>(G.total_cells * (G.p + 1));
+  t->loc = a.take<double2>(G.total_cells * (G.p + 1));
+  t->binom = a.take<double>((size_t)BS * BS);
+  t->status = a.take<DevStatus>(1);
+}
+
+
+int free_tree(fmm_tree_s* t) {
+  if (!t) return FMM_OK;
+  cudaStream_t s = t->stream;
+  if (t->scratch) cudaFreeAsync(t->scratch, s);
+  for (int i = 0; i < 3; ++i)
+    if (t->staging[i]) cudaFreeAsync(t->staging[i], s);
+  if (t->slab) cudaFreeAsync(t->slab, s);
+  for (int i = 0; i < 8; ++i)
+    if (t->ev[i]) cudaEventDestroy(t->ev[i]);
+  delete t;
+  return FMM_OK;
+}
+
+int stage_input(fmm_tree_s* t, const double* src, size_t bytes, int slot, const double** out) {
+  if (bytes == 0 || src == nullptr) {
+    *out = src;
+    return FMM_OK;
+  }
+  if (is_device_ptr(src)) {
+    *out = src;
+    return FMM_OK;
+  }
+  if (t->staging[slot]) cudaFreeAsync(t->staging[slot], t->stream);
+  t->staging[slot] = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&t->staging[slot], bytes, t->stream));
+  FMM_CUDA_TRY(cudaMemcpyAsync(t->staging[slot], src, bytes, cudaMemcpyHostToDevice, t->stream));
+  *out = t->staging[slot];
+  return FMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmm_version(void) { return 1; }
+
+const char* fmm_error_string(int code) {
+  switch (code) {
+    case FMM_OK: return "ok";
+    case FMM_EBADCFG: return "invalid configuration or argument";
+    case FMM_EDOMAIN: return "point outside the root domain";
+    case FMM_ECOINCIDENT: return "target coincides with a source";
+    case FMM_ECUDA: return "CUDA error";
+    case FMM_ENOMEM: return "device allocation failed";
+    case FMM_EEXTENSION: return "unsupported request";
+    default: return "unknown error";
+  }
+}
+
+const char* fmm_last_error_message(void) { return g_last_msg.c_str(); }
+
+int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* src_u, int64_t n,
+                   const double* tgt_xy, int64_t m, void* stream, fmm_tree_t* out) {
+  if (!out) return FMM_EBADCFG;
+  *out = nullptr;
+  Geo g;
+  int e = make_geo(cfg, &g);
+  if (e) return e;
+  if (n < 0 || m < 0 || n >= ((int64_t)1 << 31) - 64 || m >= ((int64_t)1 << 31) - 64) return FMM_EBADCFG;
+  if (cfg->self_mode) {
+    if (m != n && m != 0 && tgt_xy) return FMM_EBADCFG;
+    m = n;
+  }
+  if ((n > 0 && (!src_xy || !src_u)) || (!cfg->self_mode && m > 0 && !tgt_xy)) return FMM_EBADCFG;
+  init_pool_once();
+  fmm_tree_s* t = new fmm_tree_s();
+  memset((void*)t, 0, sizeof(*t));
+  t->cfg = *cfg;
+  t->g = g;
+  t->stream = (cudaStream_t)stream;
+  t->n = n;
+  t->m = m;
+  t->leaf_lo = g.K * cfg->rank / cfg->nranks;
+  t->leaf_hi = g.K * (cfg->rank + 1) / cfg->nranks;
+  cudaStream_t s = t->stream;
+  // inputs
+  e = stage_input(t, src_xy, (size_t)n * 16, 0, &t->src_xy_in);
+  if (!e) e = stage_input(t, src_u, (size_t)n * 8, 1, &t->src_u_in);
+  if (!e && !g.self_mode) e = stage_input(t, tgt_xy, (size_t)m * 16, 2, &t->tgt_xy_in);
+  if (e) {
+    free_tree(t);
+    return e;
+  }
+  // one slab for every tree buffer
+  Arena sizer;
+  carve(t, sizer);
+  char* slab = nullptr;
+  cudaError_t ce = cudaMallocAsync((void**)&slab, sizer.off, s);
+  if (ce != cudaSuccess) {
+    fmm_set_error_message(std::string("cudaMallocAsync slab: ") + cudaGetErrorString(ce));
+    free_tree(t);
+    return ce == cudaErrorMemoryAllocation ? FMM_ENOMEM : FMM_ECUDA;
+  }
+  Arena a;
+  a.base = slab;
+  carve(t, a);
+  t->slab = slab;
+  static std::vector<double> hb = host_binom();
+  ce = cudaMemcpyAsync(t->binom, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(t->status, 0xff, sizeof(DevStatus), s);
+  if (ce != cudaSuccess) {
+    fmm_set_error_message(cudaGetErrorString(ce));
+    free_tree(t);
+    return FMM_ECUDA;
+  }
+  e = fmm_stage_keys_sort(t);
+  if (!e) e = fmm_stage_tables_lists(t);
+  if (!e) e = fmm_build_tasks(t);
+  if (e) {
+    free_tree(t);
+    return e;
+  }
+  *out = t;
+  return FMM_OK;
+}
+
+int fmm_set_strengths(fmm_tree_t t, const double* src_u, void* stream) {
+  if (!t || (t->n > 0 && !src_u)) return FMM_EBADCFG;
+  if (stream) t->stream = (cudaStream_t)stream;
+  const double* u = nullptr;
+  int e = stage_input(t, src_u, (size_t)t->n * 8, 1, &u);
+  if (!e) e = fmm_stage_gather_strengths(t, u);
+  return e;
+}
+
+int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
+  if (!t) return FMM_EBADCFG;
+  if (stream) t->stream = (cudaStream_t)stream;
+  cudaStream_t s = t->stream;
+  if (t->m == 0) return FMM_OK;
+  if (!phi_out) return FMM_EBADCFG;
+  bool dev = is_device_ptr(phi_out);
+  double2* phi = (double2*)phi_out;
+  double2* tmp = nullptr;
+  if (!dev) {
+    FMM_CUDA_TRY(cudaMallocAsync((void**)&tmp, (size_t)t->m * 16, s));
+    phi = tmp;
+    // other ranks' targets are not written: keep the caller's values for them
+    if (t->cfg.nranks > 1)
+      FMM_CUDA_TRY(cudaMemcpyAsync(tmp, phi_out, (size_t)t->m * 16, cudaMemcpyHostToDevice, s));
+  }
+  if (t->timing) cudaEventRecord(t->ev[3], s);
+  int e = fmm_stage_upward(t);
+  if (t->timing) cudaEventRecord(t->ev[4], s);
+  if (!e) e = fmm_stage_downward(t);
+  if (t->timing) cudaEventRecord(t->ev[5], s);
+  if (!e) e = fmm_stage_p2p(t, phi);
+  if (t->timing) cudaEventRecord(t->ev[6], s);
+  if (!e && !dev) FMM_CUDA_TRY(cudaMemcpyAsync(phi_out, tmp, (size_t)t->m * 16, cudaMemcpyDeviceToHost, s));
+  if (tmp) cudaFreeAsync(tmp, s);
+  return e;
+}
+
+int fmm_status(fmm_tree_t t) {
+  if (!t) return FMM_EBADCFG;
+  FMM_CUDA_TRY(cudaStreamSynchronize(t->stream));
+  DevStatus st;
+  FMM_CUDA_TRY(cudaMemcpy(&st, t->status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st.domain_bad != ~0ull) return FMM_EDOMAIN;
+  if (st.coincident_bad != ~0ull) return FMM_ECOINCIDENT;
+  return FMM_OK;
+}
+
+int64_t fmm_last_error_index(fmm_tree_t t) {
+  if (!t) return -1;
+  if (cudaStreamSynchronize(t->stream) != cudaSuccess) return -1;
+  DevStatus st;
+  if (cudaMemcpy(&st, t->status, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (st.domain_bad != ~0ull) return (int64_t)st.domain_bad;
+  if (st.coincident_bad != ~0ull) return (int64_t)st.coincident_bad;
+  return -1;
+}
+
+int fmm_set_timing(fmm_tree_t t, int32_t enable) {
+  if (!t) return FMM_EBADCFG;
+  if (enable && !t->ev[0])
+    for (int i = 0; i < 8; ++i) FMM_CUDA_TRY(cudaEventCreate(&t->ev[i]));
+  t->timing = enable;
+  return FMM_OK;
+}
+/* evaluate-stage times of the last fmm_evaluate with timing on: {0, 0, 0, upward, downward, p2p}
+ * (build stages are timed by the caller around fmm_build_tree) */
+int fmm_stage_times(fmm_tree_t t, float* ms6) {
+  if (!t || !ms6) return FMM_EBADCFG;
+  for (int i = 0; i < 6; ++i) ms6[i] = 0.f;
+  if (!t->timing) return FMM_OK;
+  FMM_CUDA_TRY(cudaEventSynchronize(t->ev[6]));
+  cudaEventElapsedTime(&ms6[3], t->ev[3], t->ev[4]);
+  cudaEventElapsedTime(&ms6[4], t->ev[4], t->ev[5]);
+  cudaEventElapsedTime(&ms6[5], t->ev[5], t->ev[6]);
+  return FMM_OK;
+}
+
+int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi) {
+  if (!t) return FMM_EBADCFG;
+  if (lo) *lo = t->leaf_lo;
+  if (hi) *hi = t->leaf_hi;
+  return FMM_OK;
+}
+
+int64_t fmm_launch_count(fmm_tree_t t) { return t ? t->launches : -1; }
+
+void fmm_free(fmm_tree_t t) { free_tree(t); }
+
+static int copy_out(const void* src_dev, size_t bytes, void* host_buf, size_t cap, size_t* needed) {
+  if (needed) *needed = bytes;
+  if (host_buf && bytes) FMM_CUDA_TRY(cudaMemcpy(host_buf, src_dev, std::min(bytes, cap), cudaMemcpyDeviceToHost));
+  return FMM_OK;
+}
+static int copy_host(const void* src, size_t bytes, void* host_buf, size_t cap, size_t* needed) {
+  if (needed) *needed = bytes;
+  if (host_buf && bytes) memcpy(host_buf, src, std::min(bytes, cap));
+  return FMM_OK;
+}
+
+int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t bytes, size_t* needed) {
+  if (!t) return FMM_EBADCFG;
+  FMM_CUDA_TRY(cudaStreamSynchronize(t->stream));
+  const Geo& G = t->g;
+  int64_t K = G.K;
+  if ((what == FMM_X_CENTRES || what == FMM_X_E4_OWNERS || what == FMM_X_E4_OFFSETS || what == FMM_X_E4_ENTRIES ||
+       what == FMM_X_MULTIPOLE || what == FMM_X_LOCAL) &&
+      (level < 0 || level > G.L))
+    return FMM_EBADCFG;
+  switch (what) {
+    case FMM_X_SRC_KEYS: return copy_out(t->skey, (size_t)t->n * 4, host_buf, bytes, needed);
+    case FMM_X_TGT_KEYS: return copy_out(t->tkey, (size_t)t->m * 4, host_buf, bytes, needed);
+    case FMM_X_SRC_PERM: return copy_out(t->sperm, (size_t)t->n * 4, host_buf, bytes, needed);
+    case FMM_X_TGT_PERM: return copy_out(t->tperm, (size_t)t->m * 4, host_buf, bytes, needed);
+    case FMM_X_CENTRES:
+      return copy_out(t->centre + G.lvl_off[level], (size_t)G.ncells[level] * 16, host_buf, bytes, needed);
+    case FMM_X_MULTIPOLE:
+      return copy_out(t->mp + G.lvl_off[level] * (G.p + 1), (size_t)G.ncells[level] * (G.p + 1) * 16, host_buf,
+                      bytes, needed);
+    case FMM_X_LOCAL:
+      return copy_out(t->loc + G.lvl_off[level] * (G.p + 1), (size_t)G.ncells[level] * (G.p + 1) * 16, host_buf,
+                      bytes, needed);
+    default: break;
+  }
+  // host-side views that need the CSR offsets
+  std::vector<int32_t> so(K + 2), to(K + 2);
+  FMM_CUDA_TRY(cudaMemcpy(so.data(), t->soff, (K + 2) * 4, cudaMemcpyDeviceToHost));
+  FMM_CUDA_TRY(cudaMemcpy(to.data(), t->toff, (K + 2) * 4, cudaMemcpyDeviceToHost));
+  if (what == FMM_X_SRC_OFFSETS || what == FMM_X_TGT_OFFSETS) {
+    std::vector<int64_t> o(K + 1);
+    const std::vector<int32_t>& src = what == FMM_X_SRC_OFFSETS ? so : to;
+    for (int64_t i = 0; i <= K; ++i) o[i] = src[i];
+    return copy_host(o.data(), o.size() * 8, host_buf, bytes, needed);
+  }
+  auto tcount = [&](int l, int64_t c) -> int64_t {
+    int64_t span = ipow64(G.B, G.L - l);
+    int64_t lo = std::max(c * span, t->leaf_lo), hi = std::min((c + 1) * span, t->leaf_hi);
+    return hi > lo ? to[hi] - to[lo] : 0;
+  };
+  std::vector<int32_t> owners, entries;
+  std::vector<int64_t> offs(1, 0);
+  int64_t m2l_ops = 0, p2p_pairs = 0, ne_src = 0, ne_tgt = 0;
+  bool want_near = what == FMM_X_NEAR_OWNERS || what == FMM_X_NEAR_OFFSETS || what == FMM_X_NEAR_ENTRIES;
+  bool want_e4 = what == FMM_X_E4_OWNERS || what == FMM_X_E4_OFFSETS || what == FMM_X_E4_ENTRIES;
+  if (want_near || what == FMM_X_COUNTERS) {
+    std::vector<int32_t> nr(K * FMM_NEAR_MAX), nn(K);
+    FMM_CUDA_TRY(cudaMemcpy(nr.data(), t->near, nr.size() * 4, cudaMemcpyDeviceToHost));
+    FMM_CUDA_TRY(cudaMemcpy(nn.data(), t->nnear, nn.size() * 4, cudaMemcpyDeviceToHost));
+    for (int64_t leaf = 0; leaf < K; ++leaf) ne_src += so[leaf + 1] > so[leaf];
+    for (int64_t leaf = t->leaf_lo; leaf < t->leaf_hi; ++leaf) {
+      int64_t nt = to[leaf + 1] - to[leaf];
+      if (nt == 0) continue;
+      ++ne_tgt;
+      owners.push_back((int32_t)leaf);
+      int64_t ns = 0;
+      for (int q = 0; q < nn[leaf]; ++q) {
+        int32_t s = nr[leaf * FMM_NEAR_MAX + q];
+        entries.push_back(s);
+        ns += so[s + 1] - so[s];
+      }
+      p2p_pairs += nt * ns - (G.self_mode ? nt : 0);
+      offs.push_back((int64_t)entries.size());
+    }
+  }
+  if (want_e4 || what == FMM_X_COUNTERS) {
+    int l0 = want_e4 ? level : 1, l1 = want_e4 ? level : G.L;
+    if (want_e4) {
+      owners.clear();
+      entries.clear();
+      offs.assign(1, 0);
+    }
+    for (int l = std::max(l0, 1); l <= l1; ++l) {
+      int64_t nc = G.ncells[l], np = G.ncells[l - 1];
+      std::vector<int32_t> cand(np * FMM_CAND_MAX), ncand(np);
+      std::vector<unsigned long long> mask(nc);
+      FMM_CUDA_TRY(cudaMemcpy(cand.data(), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX, cand.size() * 4,
+                              cudaMemcpyDeviceToHost));
+      FMM_CUDA_TRY(cudaMemcpy(ncand.data(), t->ncand + G.lvl_off[l - 1], np * 4, cudaMemcpyDeviceToHost));
+      FMM_CUDA_TRY(cudaMemcpy(mask.data(), t->e4mask + G.lvl_off[l], nc * 8, cudaMemcpyDeviceToHost));
+      for (int64_t c = 0; c < nc; ++c) {
+        if (tcount(l, c) == 0) continue;
+        int64_t P = c / G.B;
+        unsigned long long mk = mask[c];
+        if (want_e4) owners.push_back((int32_t)c);
+        for (int i = 0; i < ncand[P] && i < 64; ++i)
+          if (mk >> i & 1ull) {
+            ++m2l_ops;
+            if (want_e4) entries.push_back(cand[P * FMM_CAND_MAX + i]);
+          }
+        if (want_e4) offs.push_back((int64_t)entries.size());
+      }
+    }
+  }
+  switch (what) {
+    case FMM_X_NEAR_OWNERS:
+    case FMM_X_E4_OWNERS: return copy_host(owners.data(), owners.size() * 4, host_buf, bytes, needed);
+    case FMM_X_NEAR_OFFSETS:
+    case FMM_X_E4_OFFSETS: return copy_host(offs.data(), offs.size() * 8, host_buf, bytes, needed);
+    case FMM_X_NEAR_ENTRIES:
+    case FMM_X_E4_ENTRIES: return copy_host(entries.data(), entries.size() * 4, host_buf, bytes, needed);
+    case FMM_X_COUNTERS: {
+      int64_t c[4] = {m2l_ops, p2p_pairs, ne_src, ne_tgt};
+      return copy_host(c, sizeof(c), host_buf, bytes, needed);
+    }
+    default: return FMM_EBADCFG;
+  }
+}
+
+}  // extern "C"

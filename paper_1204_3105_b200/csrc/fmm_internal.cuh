@@ -1,0 +1,111 @@
+// fmm_internal.cuh -- shared definitions of the B200 FMM library (CUDA, sm_100a).
+// Product code only; never includes anything from oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fmm_b200.h"
+
+#define FMM_MAX_P 32
+#define FMM_CAND_MAX 64  // >= 4*13 (triangle), 7*7 (septree), 4*9 (quad) E4 candidates per sibling group
+#define FMM_NEAR_MAX 16  // >= 13 (triangle near set incl. self)
+
+// ---------------------------------------------------------------- host-side geometry constants
+struct Geo {
+  int tiling, L, B, p, self_mode;
+  int64_t K;              // B^L leaves
+  int64_t ncells[17];     // B^l
+  int64_t lvl_off[18];    // start of level l in the all-level cell arrays
+  int64_t total_cells;
+  double root_x, root_y, root_size;
+  // septree: leaf circumradius and lattice factors (D8, D11)
+  double sept_r, sept_A, sept_Bc, sept_D3r;
+  int sept_K;             // |lattice coordinate| bound for in-domain points
+};
+
+struct DevStatus {
+  unsigned long long domain_bad;      // min offending index (ULLONG_MAX = none)
+  unsigned long long coincident_bad;  // min offending target index
+};
+
+struct fmm_tree_s {
+  fmm_config cfg;
+  Geo g;
+  cudaStream_t stream;
+  int64_t n, m;
+  int own_inputs;
+  // inputs (device)
+  const double* src_xy_in;  // interleaved
+  const double* src_u_in;
+  const double* tgt_xy_in;
+  double* staging[3];       // device copies of host inputs (or NULL)
+  // keys / permutation / CSR
+  uint32_t* skey;  // [n]
+  uint32_t* tkey;  // [m] (aliases skey in self mode)
+  int32_t* sperm;  // [n] sorted position -> input index
+  int32_t* tperm;  // [m]
+  int32_t* soff;   // [K+2]
+  int32_t* toff;   // [K+2]
+  // sorted data
+  double2* sxy;    // [n]
+  double* su;      // [n]
+  double2* txy;    // [m] (aliases sxy in self mode)
+  // tree tables
+  double2* centre; // [total_cells]
+  int32_t* cand;   // [cells of levels 0..L-1][FMM_CAND_MAX]  E4 candidates of each parent, ascending
+  int32_t* ncand;  // [cells of levels 0..L-1]
+  unsigned long long* e4mask; // [total_cells] bit i <=> cand[parent][i] in E4(cell)
+  int32_t* near;   // [K][FMM_NEAR_MAX]
+  int32_t* nnear;  // [K]
+  // P2P work list
+  int32_t* task_leaf;  // [ntask_cap]
+  int32_t* task_start; // [ntask_cap] sorted target position of the chunk start
+  int32_t* ntask;      // [1] device counter
+  int64_t ntask_cap;
+  // expansions
+  double2* mp;     // [total_cells][p+1]
+  double2* loc;    // [total_cells][p+1]
+  double* binom;   // [(2P+1)][(2P+1)] binomial table
+  // status
+  DevStatus* status;
+  // multi-rank leaf range
+  int64_t leaf_lo, leaf_hi;
+  // timing
+  int timing;
+  cudaEvent_t ev[8];
+  float stage_ms[6];
+  int64_t launches;
+  void* slab;  // single allocation holding every tree buffer
+  // scratch for sort
+  void* scratch;
+  size_t scratch_bytes;
+};
+
+// ---------------------------------------------------------------- error helpers
+void fmm_set_error_message(const std::string& s);
+#define FMM_CUDA_TRY(expr)                                                                         \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess) {                                                                       \
+      fmm_set_error_message(std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+      return _e == cudaErrorMemoryAllocation ? FMM_ENOMEM : FMM_ECUDA;                             \
+    }                                                                                              \
+  } while (0)
+
+// ---------------------------------------------------------------- stage entry points (host)
+// build.cu
+int fmm_stage_keys_sort(fmm_tree_s* t);
+int fmm_stage_tables_lists(fmm_tree_s* t);
+int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
+                        cudaStream_t s, int64_t* launches);
+size_t fmm_scan_scratch_bytes(int64_t n);
+// passes.cu
+int fmm_stage_upward(fmm_tree_s* t);
+int fmm_stage_downward(fmm_tree_s* t);
+int fmm_stage_p2p(fmm_tree_s* t, double2* phi_out);
+int fmm_build_tasks(fmm_tree_s* t);
+int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);

@@ -1,0 +1,206 @@
+"""ctypes binding of libfmm_b200.so (include/fmm_b200.h): names mirror the C ABI.
+
+Inputs may be torch tensors (CUDA -> device pointers used in place; CPU ->
+host pointers staged by the library) or numpy arrays (host).  Argument
+marshalling only; no arithmetic of the method happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libfmm_b200.so")
+
+QUADTREE, SEPTREE, TRIQUAD = 0, 1, 2
+_TILING = {"quad": QUADTREE, "sept": SEPTREE, "triq": TRIQUAD, QUADTREE: 0, SEPTREE: 1, TRIQUAD: 2}
+
+
+class X:
+    """export selectors (FMM_X_*)"""
+    SRC_KEYS, TGT_KEYS, SRC_PERM, TGT_PERM, SRC_OFFSETS, TGT_OFFSETS = 1, 2, 3, 4, 5, 6
+    CENTRES, NEAR_OWNERS, NEAR_OFFSETS, NEAR_ENTRIES = 7, 8, 9, 10
+    E4_OWNERS, E4_OFFSETS, E4_ENTRIES, MULTIPOLE, LOCAL, COUNTERS = 11, 12, 13, 14, 15, 16
+
+
+_DTYPE = {X.SRC_KEYS: np.uint32, X.TGT_KEYS: np.uint32, X.SRC_PERM: np.int32, X.TGT_PERM: np.int32,
+          X.SRC_OFFSETS: np.int64, X.TGT_OFFSETS: np.int64, X.CENTRES: np.float64, X.NEAR_OWNERS: np.int32,
+          X.NEAR_OFFSETS: np.int64, X.NEAR_ENTRIES: np.int32, X.E4_OWNERS: np.int32, X.E4_OFFSETS: np.int64,
+          X.E4_ENTRIES: np.int32, X.MULTIPOLE: np.complex128, X.LOCAL: np.complex128, X.COUNTERS: np.int64}
+
+
+class Config(C.Structure):
+    _fields_ = [("tiling", C.c_int32), ("depth", C.c_int32), ("p", C.c_int32), ("self_mode", C.c_int32),
+                ("root_x", C.c_double), ("root_y", C.c_double), ("root_size", C.c_double),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("reserved", C.c_int32 * 6)]
+
+    @classmethod
+    def make(cls, tiling, depth, p, root_x, root_y, root_size, self_mode=False, rank=0, nranks=1):
+        return cls(_TILING[tiling], int(depth), int(p), int(bool(self_mode)), float(root_x), float(root_y),
+                   float(root_size), int(rank), int(nranks))
+
+
+class FmmError(RuntimeError):
+    def __init__(self, code, what="", index=-1):
+        msg = lib().fmm_error_string(code).decode()
+        extra = lib().fmm_last_error_message().decode()
+        super().__init__(f"{what}: FMM error {code} ({msg}) {extra} index={index}")
+        self.code = code
+        self.index = index
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _SO
+
+
+def lib():
+    """load libfmm_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(_SO)
+        P = C.POINTER
+        vp, d = C.c_void_p, P(C.c_double)
+        sig = {
+            "fmm_build_tree": (C.c_int, [P(Config), vp, vp, C.c_int64, vp, C.c_int64, vp, P(vp)]),
+            "fmm_evaluate": (C.c_int, [vp, vp, vp]),
+            "fmm_set_strengths": (C.c_int, [vp, vp, vp]),
+            "fmm_status": (C.c_int, [vp]),
+            "fmm_last_error_index": (C.c_int64, [vp]),
+            "fmm_export": (C.c_int, [vp, C.c_int32, C.c_int32, vp, C.c_size_t, P(C.c_size_t)]),
+            "fmm_set_timing": (C.c_int, [vp, C.c_int32]),
+            "fmm_stage_times": (C.c_int, [vp, P(C.c_float)]),
+            "fmm_rank_range": (C.c_int, [vp, P(C.c_int64), P(C.c_int64)]),
+            "fmm_launch_count": (C.c_int64, [vp]),
+            "fmm_free": (None, [vp]),
+            "fmm_error_string": (C.c_char_p, [C.c_int]),
+            "fmm_last_error_message": (C.c_char_p, []),
+            "fmm_version": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    """(pointer, keepalive) for a torch tensor or numpy array (None -> NULL)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return C.c_void_p(a.data_ptr()), a
+    a = np.ascontiguousarray(a)
+    return C.c_void_p(a.ctypes.data), a
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Tree:
+    """fmm_tree_t: built by fmm_build_tree, evaluated by fmm_evaluate."""
+
+    def __init__(self, cfg: Config, src_xy, src_u, tgt_xy=None, stream=None):
+        self.cfg = cfg
+        n = int(src_u.shape[0])
+        m = n if cfg.self_mode else int(tgt_xy.shape[0])
+        self.n, self.m = n, m
+        ps, ks = _ptr(src_xy)
+        pu, ku = _ptr(src_u)
+        pt, kt = _ptr(None if cfg.self_mode else tgt_xy)
+        self._keep = (ks, ku, kt)
+        self._stream = _stream_ptr(stream)
+        h = C.c_void_p()
+        rc = lib().fmm_build_tree(C.byref(cfg), ps, pu, n, pt, m, self._stream, C.byref(h))
+        if rc:
+            raise FmmError(rc, "fmm_build_tree")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fmm_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def evaluate(self, out=None, stream=None):
+        """Phi as complex128 [m] in the caller's target order (torch CUDA tensor by default)."""
+        if out is None:
+            import torch
+
+            out = torch.zeros(self.m, dtype=torch.complex128, device="cuda")
+        po, ko = _ptr(out)
+        st = _stream_ptr(stream) if stream is not None else self._stream
+        rc = lib().fmm_evaluate(self.h, po, st)
+        if rc:
+            raise FmmError(rc, "fmm_evaluate")
+        return out
+
+    def set_strengths(self, u, stream=None):
+        pu, ku = _ptr(u)
+        rc = lib().fmm_set_strengths(self.h, pu, _stream_ptr(stream) if stream is not None else self._stream)
+        if rc:
+            raise FmmError(rc, "fmm_set_strengths")
+        self._keep = self._keep + (ku,)
+
+    def status(self):
+        rc = lib().fmm_status(self.h)
+        return rc, int(lib().fmm_last_error_index(self.h))
+
+    def check(self):
+        rc, idx = self.status()
+        if rc:
+            raise FmmError(rc, "device status", idx)
+
+    def export(self, what, level=0):
+        need = C.c_size_t()
+        rc = lib().fmm_export(self.h, what, level, None, 0, C.byref(need))
+        if rc:
+            raise FmmError(rc, "fmm_export")
+        dt = np.dtype(_DTYPE[what])
+        buf = np.empty(need.value // dt.itemsize, dtype=dt)
+        rc = lib().fmm_export(self.h, what, level, C.c_void_p(buf.ctypes.data), buf.nbytes, C.byref(need))
+        if rc:
+            raise FmmError(rc, "fmm_export")
+        return buf
+
+    def set_timing(self, on=True):
+        lib().fmm_set_timing(self.h, int(on))
+
+    def stage_times(self):
+        ms = (C.c_float * 6)()
+        lib().fmm_stage_times(self.h, ms)
+        return list(ms)
+
+    def rank_range(self):
+        lo, hi = C.c_int64(), C.c_int64()
+        lib().fmm_rank_range(self.h, C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
+
+    def launch_count(self):
+        return int(lib().fmm_launch_count(self.h))

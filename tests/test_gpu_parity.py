@@ -1,0 +1,192 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle on the
+same seeded inputs.  Bit-exact: keys, sort permutation, leaf CSR, centres, near and
+E4 lists.  Floating point: multipoles and potentials within 1e-12 normwise (D15)."""
+import numpy as np
+import pytest
+
+from gpu_common import SMALL_CASES, data, gpu_tree, normwise, oracle_tree
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12  # BASELINE.json north_star: <= 1e-12 relative against the oracle FMM (normwise, D15)
+
+
+@pytest.fixture(scope="module")
+def pair_cache():
+    return {}
+
+
+def pair(cache, name):
+    if name not in cache:
+        w = SMALL_CASES[name]
+        d = data(w)
+        g = gpu_tree(w, d)
+        o = oracle_tree(w, d)
+        phi = g.evaluate()
+        g.check()
+        cache[name] = (w, d, g, o, phi.cpu().numpy())
+    return cache[name]
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_keys_perm_offsets_bit_exact(pair_cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = pair(pair_cache, name)
+    sk, tk = o.keys()
+    sp, tp = o.perm()
+    so, to = o.leaf_offsets()
+    assert np.array_equal(g.export(X.SRC_KEYS), sk)
+    assert np.array_equal(g.export(X.SRC_PERM), sp)
+    assert np.array_equal(g.export(X.SRC_OFFSETS), so)
+    if not w.self_mode:
+        assert np.array_equal(g.export(X.TGT_KEYS), tk)
+        assert np.array_equal(g.export(X.TGT_PERM), tp)
+        assert np.array_equal(g.export(X.TGT_OFFSETS), to)
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_centres_bit_exact(pair_cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = pair(pair_cache, name)
+    for l in range(w.depth + 1):
+        gc = g.export(X.CENTRES, l).reshape(-1, 2)
+        oc = o.centres(l)
+        assert np.array_equal(gc.view(np.uint64), oc.view(np.uint64)), l
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_lists_bit_exact(pair_cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = pair(pair_cache, name)
+    ow, of, en = o.near_csr()
+    assert np.array_equal(g.export(X.NEAR_OWNERS), ow)
+    assert np.array_equal(g.export(X.NEAR_OFFSETS), of)
+    assert np.array_equal(g.export(X.NEAR_ENTRIES), en)
+    for l in range(1, w.depth + 1):
+        ow, of, en = o.e4_csr(l)
+        assert np.array_equal(g.export(X.E4_OWNERS, l), ow), l
+        assert np.array_equal(g.export(X.E4_OFFSETS, l), of), l
+        assert np.array_equal(g.export(X.E4_ENTRIES, l), en), l
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_multipoles(pair_cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = pair(pair_cache, name)
+    for l in range(1, w.depth + 1):
+        gm = g.export(X.MULTIPOLE, l).reshape(-1, w.p + 1)
+        om = o.multipoles(l)
+        assert normwise(gm, om) <= TOL, l
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_potentials(pair_cache, name):
+    w, d, g, o, phi = pair(pair_cache, name)
+    ref, cnt = o.evaluate(counters=True)
+    assert normwise(phi, ref) <= TOL
+    from paper_1204_3105_b200 import X
+
+    c = g.export(X.COUNTERS)
+    assert c[0] == cnt["m2l_ops"] and c[1] == cnt["p2p_pairs"]
+
+
+def test_host_inputs_match_device_inputs():
+    w = SMALL_CASES["C1"]
+    d = data(w)
+    a = gpu_tree(w, d).evaluate().cpu().numpy()
+    out = np.zeros(w.m, np.complex128)
+    gh = gpu_tree(w, d, host_inputs=True)
+    gh.evaluate(out)
+    import torch
+
+    torch.cuda.synchronize()
+    assert np.array_equal(a, out)
+
+
+@pytest.mark.parametrize("p", [1, 5, 31])
+def test_expansion_orders(p):
+    w = SMALL_CASES["C2"].scaled(3000)
+    d = data(w)
+    phi = gpu_tree(w, d, p=p).evaluate().cpu().numpy()
+    assert normwise(phi, oracle_tree(w, d, p=p).evaluate()) <= TOL
+
+
+@pytest.mark.parametrize("tiling_case", ["C1", "C2", "C4qs"])
+def test_depth_one(tiling_case):
+    w = SMALL_CASES[tiling_case].scaled(2000, name=tiling_case + "-L1")
+    w.depth = 1  # the septree island of depth 1 is the 7-hexagon flower: regenerate inside it
+    d = data(w)
+    phi = gpu_tree(w, d).evaluate().cpu().numpy()
+    assert normwise(phi, oracle_tree(w, d).evaluate()) <= TOL
+
+
+def test_empty_sources_and_targets():
+    import torch
+
+    from paper_1204_3105_b200 import Config, Tree
+
+    w = SMALL_CASES["C1"]
+    cfg = Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, False)
+    t = Tree(cfg, torch.zeros((0, 2), dtype=torch.float64, device="cuda"),
+             torch.zeros(0, dtype=torch.float64, device="cuda"),
+             torch.tensor([[0.01, 0.02], [0.1, -0.2]], dtype=torch.float64, device="cuda"))
+    phi = t.evaluate().cpu().numpy()
+    t.check()
+    assert np.all(phi == 0)
+    t2 = Tree(cfg, torch.tensor([[0.01, 0.02]], dtype=torch.float64, device="cuda"),
+              torch.ones(1, dtype=torch.float64, device="cuda"), torch.zeros((0, 2), dtype=torch.float64, device="cuda"))
+    assert t2.evaluate().numel() == 0
+
+
+def test_out_of_domain_reported():
+    import torch
+
+    from paper_1204_3105_b200 import Config, FmmError, Tree
+
+    w = SMALL_CASES["C1"]
+    cfg = Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, True)
+    xy = torch.tensor([[0.0, 0.0], [0.1, 0.1], [3.0, 0.0], [0.2, -0.1]], dtype=torch.float64, device="cuda")
+    t = Tree(cfg, xy, torch.ones(4, dtype=torch.float64, device="cuda"))
+    rc, idx = t.status()
+    assert rc == 2 and idx == 2
+    with pytest.raises(FmmError):
+        t.check()
+
+
+def test_coincident_reported():
+    import torch
+
+    w = SMALL_CASES["C2"].scaled(500)
+    d = dict(data(w))
+    xy = d["src_xy"].copy()
+    xy[10] = xy[3]
+    d["src_xy"] = xy
+    t = gpu_tree(w, d)
+    t.evaluate()
+    rc, idx = t.status()
+    assert rc == 3 and idx == 3
+
+
+def test_repeat_evaluate_deterministic():
+    w = SMALL_CASES["C4ts"]
+    d = data(w)
+    g = gpu_tree(w, d)
+    a = g.evaluate().cpu().numpy()
+    b = g.evaluate().cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_set_strengths_linearity():
+    import torch
+
+    w = SMALL_CASES["C2"].scaled(4000)
+    d = data(w)
+    g = gpu_tree(w, d)
+    a = g.evaluate().cpu().numpy()
+    g.set_strengths(torch.from_numpy(2.0 * d["u"]).cuda())
+    b = g.evaluate().cpu().numpy()
+    assert normwise(b, 2 * a) <= 1e-14
