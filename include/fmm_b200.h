@@ -151,6 +151,12 @@ int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi);
 int64_t fmm_launch_count(fmm_tree_t t);
 
 void fmm_free(fmm_tree_t t);
+
+/* Test hook: the P2P kernel's FP64 math on n explicit offsets z = dx + i dy (device
+ * pointers, interleaved): out[2i] = log|z|^2, out[2i+1] = Arg z in (-pi, pi] with a zero
+ * imaginary part read as +0 (D13).  z must have a normal |z|^2 (the kernel
+ * sends zero / subnormal |z|^2 to an exact slow path).  Synchronises `stream`. */
+int fmm_debug_p2p_math(const double* dxdy, int64_t n, double* out, void* stream);
 const char* fmm_error_string(int code);
 const char* fmm_last_error_message(void);
 int fmm_version(void);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "fmm_internal.cuh"
+#include "p2p_math.cuh"
 
 static thread_local std::string g_last_msg;
 void fmm_set_error_message(const std::string& s) { g_last_msg = s; }
@@ -25,6 +26,35 @@ std::vector<double> host_binom() {
   }
   return b;
 }
+
+}  // namespace
+
+// tables of p2p_math.cuh, computed once in extended precision (x87 long double)
+void fmm_host_p2p_tables(double* tab) {
+  for (int i = 0; i < P2P_LOG_N; ++i) {
+    // interval centre: the value of the centre bit pattern (exactly 1.0 for the interval of 1.0)
+    uint64_t mid = P2P_LOG_OFF + ((uint64_t)i << 45) + ((uint64_t)1 << 44);
+    double c;
+    memcpy(&c, &mid, 8);
+    double invc = 1.0 / c;
+    tab[P2P_TAB_LOG + 2 * i] = invc;
+    tab[P2P_TAB_LOG + 2 * i + 1] = (double)(-logl((long double)invc));
+  }
+  const long double PI = acosl(-1.0L);
+  for (int oct = 0; oct < 8; ++oct) {
+    int swap = oct & 1, dxneg = (oct >> 1) & 1, dyneg = (oct >> 2) & 1;
+    for (int k = 0; k <= P2P_ATAN_K; ++k) {
+      long double a = atanl((long double)k / P2P_ATAN_K);
+      long double t1 = swap ? PI / 2 - a : a;
+      long double t2 = dxneg ? PI - t1 : t1;
+      long double t3 = dyneg ? -t2 : t2;
+      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k)] = (double)t3;
+      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = (double)k / P2P_ATAN_K;
+    }
+  }
+}
+
+namespace {
 
 void init_pool_once() {
   static std::once_flag f;
@@ -140,6 +170,8 @@ void carve(fmm_tree_s* t, Arena& a) {
   t->task_leaf = a.take<int32_t>(t->ntask_cap);
   t->task_start = a.take<int32_t>(t->ntask_cap);
   t->ntask = a.take<int32_t>(1);
+  t->next_task = a.take<int32_t>(1);
+  t->p2p_tab = a.take<double>(P2P_TAB_DOUBLES);
   t->mp = a.take<double2>(G.total_cells * (G.p + 1));
   t->loc = a.take<double2>(G.total_cells * (G.p + 1));
   t->binom = a.take<double>((size_t)BS * BS);
@@ -245,7 +277,14 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   carve(t, a);
   t->slab = slab;
   static std::vector<double> hb = host_binom();
+  static std::vector<double> htab = [] {
+    std::vector<double> v(P2P_TAB_DOUBLES);
+    fmm_host_p2p_tables(v.data());
+    return v;
+  }();
   ce = cudaMemcpyAsync(t->binom, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(t->p2p_tab, htab.data(), htab.size() * sizeof(double), cudaMemcpyHostToDevice, s);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(t->status, 0xff, sizeof(DevStatus), s);
   if (ce != cudaSuccess) {
     fmm_set_error_message(cudaGetErrorString(ce));
@@ -350,6 +389,21 @@ int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi) {
 int64_t fmm_launch_count(fmm_tree_t t) { return t ? t->launches : -1; }
 
 void fmm_free(fmm_tree_t t) { free_tree(t); }
+
+int fmm_debug_p2p_math(const double* dxdy, int64_t n, double* out, void* stream) {
+  if (n <= 0) return FMM_OK;
+  if (!is_device_ptr(dxdy) || !is_device_ptr(out)) return FMM_EBADCFG;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<double> tab(P2P_TAB_DOUBLES);
+  fmm_host_p2p_tables(tab.data());
+  double* dtab = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&dtab, tab.size() * 8, s));
+  FMM_CUDA_TRY(cudaMemcpyAsync(dtab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
+  int e = fmm_debug_p2p_math_launch(dxdy, n, dtab, out, s);
+  FMM_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(dtab, s);
+  return e;
+}
 
 static int copy_out(const void* src_dev, size_t bytes, void* host_buf, size_t cap, size_t* needed) {
   if (needed) *needed = bytes;

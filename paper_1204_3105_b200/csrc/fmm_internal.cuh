@@ -65,7 +65,9 @@ struct fmm_tree_s {
   int32_t* task_leaf;  // [ntask_cap]
   int32_t* task_start; // [ntask_cap] sorted target position of the chunk start
   int32_t* ntask;      // [1] device counter
+  int32_t* next_task;  // [1] dynamic scheduling counter of the P2P kernel
   int64_t ntask_cap;
+  double* p2p_tab;     // [P2P_TAB_DOUBLES] log / atan tables of p2p_math.cuh
   // expansions
   double2* mp;     // [total_cells][p+1]
   double2* loc;    // [total_cells][p+1]
@@ -109,3 +111,6 @@ int fmm_stage_downward(fmm_tree_s* t);
 int fmm_stage_p2p(fmm_tree_s* t, double2* phi_out);
 int fmm_build_tasks(fmm_tree_s* t);
 int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);
+int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s);
+// capi.cu
+void fmm_host_p2p_tables(double* tab);  // fills P2P_TAB_DOUBLES doubles

@@ -1,0 +1,124 @@
+// p2p_math.cuh -- FP64 log|z|^2 and Arg z for the P2P near field (kernel Log(y - x)).
+//
+// Both are table-driven and accurate to ~1 ulp (absolute error below ~2^-52 max(1, |result|));
+// they replace libdevice log / atan2, whose integer, branch and polynomial work made the
+// pair loop ~4x slower.  Valid for |z| >= 1e-30 (the caller sends
+// smaller |z|, including the excluded / coincident z = 0, to an exact slow path).
+//
+//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 128-entry table of
+//            (1/c_i, log c_i) selected by the top mantissa bits; |r| < 2^-8;
+//            log1p(r) by its Taylor series to r^7 (truncation < 2^-67).
+//   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/32 with k = round(32 t)
+//            from an FP32 estimate; atan t = atan t_k + atan q,
+//            q = (num - t_k den) / (den + t_k num), |q| <= 1/64 + 2^-20;
+//            atan q = q - q^3/3 + q^5/5 - q^7/7 + q^9/9 (truncation < 2^-66 |q|);
+//            the octant's offset and sign are folded into a table T[oct][k].
+//   division: MUFU.RCP64H estimate + one cubic Newton step (e + e^2), error ~ e^3.
+// Polynomial coefficients live in the constant bank (DFMA operands, no register moves).
+#pragma once
+#include <stdint.h>
+
+#define P2P_LOG_N 128
+#define P2P_ATAN_K 32  // t_k = k / 32, k = 0..32
+// table layout (doubles): [0, 256) log (1/c, log c) pairs; [256, 256 + 2*8*33) (T[oct][k], t_k)
+#define P2P_TAB_LOG 0
+#define P2P_TAB_ATAN 256
+#define P2P_TAB_DOUBLES (256 + 2 * 8 * (P2P_ATAN_K + 1))
+// |z|^2 below this (hi word of 1e-60) takes the exact slow path
+#define P2P_SLOW_HI 0x3379b604
+// z intervals: bit patterns [OFF + i 2^45, OFF + (i+1) 2^45), OFF = 0x3fe6000000000000 - 2^44,
+// so that the bit pattern of 1.0 is the centre of interval 80
+#define P2P_LOG_OFF_HI 0x3fe5f000
+#define P2P_LOG_OFF 0x3fe5f00000000000ull
+
+__constant__ double P2P_C[12] = {
+    1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,  // log1p Taylor r^7 .. r^2
+    1.0 / 9.0, -1.0 / 7.0, 1.0 / 5.0, -1.0 / 3.0,                   // atan Taylor q^9 .. q^3
+    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45                      // ln 2 = hi (42 bits) + lo
+};
+
+// copy the tables to shared memory (whole block; ends with __syncthreads); the math
+// functions take the tables' 32-bit shared-space addresses (hoisted out of the pair loop)
+__device__ __forceinline__ void p2p_load_tables(const double* __restrict__ tabs, double2* s_log, double2* s_atan) {
+  const double2* t2 = (const double2*)tabs;
+  for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
+  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATAN / 2 + i];
+  __syncthreads();
+}
+
+// 16-byte load from a shared-space (32-bit) address
+__device__ __forceinline__ double2 p2p_lds2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ double p2p_rcp(double b) {
+  double r0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(b));
+  double e = fma(-b, r0, 1.0);
+  e = fma(e, e, e);
+  return fma(e, r0, r0);
+}
+
+__device__ __forceinline__ float p2p_rcpf(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
+// The 128 intervals of z are centred so that z = 1 is the centre of its interval
+// (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
+__device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
+  int hi = __double2hiint(r2), lo = __double2loint(r2);
+  int tmp = hi - P2P_LOG_OFF_HI;
+  int i = (tmp >> 13) & (P2P_LOG_N - 1);
+  int k = tmp >> 20;  // arithmetic shift
+  double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
+  double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
+  double r = fma(z, cl.x, -1.0);
+  double r_2 = r * r;
+  double q = fma(r, P2P_C[0], P2P_C[1]);
+  q = fma(q, r, P2P_C[2]);
+  q = fma(q, r, P2P_C[3]);
+  q = fma(q, r, P2P_C[4]);
+  q = fma(q, r, P2P_C[5]);
+  *lz = cl.y + fma(r_2, q, r);  // log c_i + log1p(r)
+  *kd = (double)k;
+}
+
+__device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
+  double kd, lz;
+  p2p_log_split(r2, logtab, &kd, &lz);
+  return fma(kd, P2P_C[10], lz) + kd * P2P_C[11];
+}
+
+// Arg(dx + i dy) in (-pi, pi], a zero imaginary part read as +0 (D13); |z| >= 1e-30
+__device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
+  // FP32 estimate of t = min/max of |dx|, |dy| (both representable: |z| >= 1e-30)
+  float fx = fabsf(__double2float_rn(dx)), fy = fabsf(__double2float_rn(dy));
+  bool swap = fy > fx;
+  float tf = fminf(fx, fy) * p2p_rcpf(fmaxf(fx, fy));
+  int k = __float_as_int(fmaf(tf, 32.0f, 12582912.0f)) & 0x3f;  // round(32 t), 0..32
+  double num = swap ? dx : dy, den = swap ? dy : dx;
+  num = fabs(num);
+  den = fabs(den);
+  // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0 (dy = -0 counts as +0)
+  int hx = __double2hiint(dx), hy = __double2hiint(dy);
+  bool dyneg = (hy < 0) && (((hy & 0x7fffffff) | __double2loint(dy)) != 0);
+  int oct = (int)swap | ((hx >> 31) & 2) | ((int)dyneg << 2);
+  double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (T[oct][k], t_k)
+  double a = fma(-Tt.y, den, num);
+  double b = fma(Tt.y, num, den);
+  double q = a * p2p_rcp(b);
+  double q2 = q * q;
+  double P = fma(q2, P2P_C[6], P2P_C[7]);
+  P = fma(P, q2, P2P_C[8]);
+  P = fma(P, q2, P2P_C[9]);
+  double at = fma(q * q2, P, q);
+  // sign S = (-1)^(swap + dxneg + dyneg) applied by flipping the sign bit
+  int par = ((int)swap ^ (int)dyneg ^ (hx >> 31)) & 1;
+  at = __hiloint2double(__double2hiint(at) ^ (par << 31), __double2loint(at));
+  return Tt.x + at;
+}

@@ -7,8 +7,11 @@
 //        b_0  = Q Log(c_L - c_M) + sum_k (-1)^k a_k w^k
 //   L2L  b'_l = sum_{k=l..p} b_k C(k, l) w^{k-l},                      w = c_child - c_parent
 //   L2P  sum_l b_l (y - c)^l;  P2P  sum_i u_i Log(y - x_i)
+#include <stdlib.h>
+
 #include "fmm_internal.cuh"
 #include "geometry.cuh"
+#include "p2p_math.cuh"
 
 namespace {
 
@@ -205,6 +208,107 @@ __global__ void k_fill_tasks(const int32_t* __restrict__ toff, int64_t leaf_lo, 
 }
 
 // ------------------------------------------------------------------ L2P + P2P (one warp per 32-target chunk)
+// Sources of each near leaf are staged 32 at a time in shared memory (one coalesced load
+// per lane) and read back as broadcasts; log|z|^2 and Arg z come from p2p_math.cuh.
+// Tasks are claimed dynamically (one atomic per warp task) for load balance.
+__global__ void __launch_bounds__(128) k_p2p_fast(
+    const int32_t* __restrict__ task_leaf, const int32_t* __restrict__ task_start, const int32_t* __restrict__ ntask_p,
+    int32_t* __restrict__ next_task, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
+    const double2* __restrict__ txy, const double2* __restrict__ sxy, const double* __restrict__ su,
+    const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, const double2* __restrict__ cen_leaf,
+    const double2* __restrict__ loc_leaf, int p, int self_mode, const int32_t* __restrict__ tperm,
+    const double* __restrict__ tabs, double2* __restrict__ phi, DevStatus* st) {
+  __shared__ double2 s_log[P2P_LOG_N];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  __shared__ double2 s_xy[4][32];
+  __shared__ double s_u[4][32];
+  p2p_load_tables(tabs, s_log, s_atan);
+  const uint32_t a_log = (uint32_t)__cvta_generic_to_shared(s_log);
+  const uint32_t a_atan = (uint32_t)__cvta_generic_to_shared(s_atan);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ntask = *ntask_p;
+  while (true) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(next_task, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= ntask) break;
+    const int t = task_leaf[task];
+    const int tpos0 = task_start[task];
+    const int nt = min(32, toff[t + 1] - tpos0);
+    const int tpos = tpos0 + lane;
+    const bool active = lane < nt;
+    const double2 y = active ? txy[tpos] : make_double2(1.0e5, 1.0e5);
+    double re = 0.0, re_k = 0.0, im = 0.0;
+    const int nn = nnear[t];
+    for (int qn = 0; qn < nn; ++qn) {
+      const int sl = near[(int64_t)t * FMM_NEAR_MAX + qn];
+      const int s0 = soff[sl], s1 = soff[sl + 1];
+      for (int j0 = s0; j0 < s1; j0 += 32) {
+        const int j = j0 + lane;
+        if (j < s1) {
+          s_xy[w][lane] = sxy[j];
+          s_u[w][lane] = su[j];
+        }
+        __syncwarp();
+        const int cnt = min(32, s1 - j0);
+        const int excl = (self_mode && sl == t) ? (tpos - j0) : -1;
+#pragma unroll 2
+        for (int k = 0; k < cnt; ++k) {
+          const double2 x = s_xy[w][k];
+          const double uu = s_u[w][k];
+          double dx = y.x - x.x, dy = y.y - x.y;
+          // the pair (i, i) in self mode (D16): dx = dy = 0 exactly; z := 1 + 0i gives
+          // log|z|^2 = 0 and Arg z = 0 exactly, so the pair contributes nothing
+          if (k == excl) dx = 1.0;
+          const double r2 = fma(dx, dx, dy * dy);
+          double kd, lz, ag;
+          if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
+            kd = 0.0;
+            if (r2 == 0.0) {
+              if (active) atomicMin(&st->coincident_bad, (unsigned long long)tperm[tpos]);
+              lz = 0.0;
+              ag = 0.0;
+            } else {
+              lz = 2.0 * log(hypot(dx, dy));
+              ag = atan2(__dadd_rn(dy, 0.0), dx);
+            }
+          } else {
+            p2p_log_split(r2, a_log, &kd, &lz);
+            ag = p2p_atan2(dy, dx, a_atan);
+          }
+          re_k = fma(uu, kd, re_k);  // sum u k  (times ln 2 at the end)
+          re = fma(uu, lz, re);
+          im = fma(uu, ag, im);
+        }
+        __syncwarp();
+      }
+    }
+    if (active) {
+      const double2 c = cen_leaf[t];
+      const double2 z = make_double2(y.x - c.x, y.y - c.y);
+      const double2* b = loc_leaf + (int64_t)t * (p + 1);
+      double2 acc = b[p];
+      for (int k = p - 1; k >= 0; --k) acc = cadd(cmul(acc, z), b[k]);
+      re = fma(re_k, P2P_C[10], re) + re_k * P2P_C[11];  // + ln 2 * sum u k
+      phi[tperm[tpos]] = make_double2(acc.x + 0.5 * re, acc.y + im);
+    }
+  }
+}
+
+// debug hook: the P2P math on explicit (dx, dy) pairs -> (log |z|^2, Arg z)
+__global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
+                                 double2* __restrict__ out) {
+  __shared__ double2 s_log[P2P_LOG_N];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  p2p_load_tables(tabs, s_log, s_atan);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double dx = d[i].x, dy = d[i].y;
+  double r2 = fma(dx, dx, dy * dy);
+  out[i] = make_double2(p2p_log(r2, (uint32_t)__cvta_generic_to_shared(s_log)),
+                        p2p_atan2(dy, dx, (uint32_t)__cvta_generic_to_shared(s_atan)));
+}
+
 __global__ void __launch_bounds__(128) k_p2p(const int32_t* __restrict__ task_leaf, const int32_t* __restrict__ task_start,
                                              const int32_t* __restrict__ ntask_p, const int32_t* __restrict__ toff,
                                              const int32_t* __restrict__ soff, const double2* __restrict__ txy,
@@ -341,11 +445,27 @@ int fmm_build_tasks(fmm_tree_s* t) {
 int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   const Geo& G = t->g;
   cudaStream_t s = t->stream;
-  int blocks = 148 * 32;
-  k_p2p<<<blocks, 128, 0, s>>>(t->task_leaf, t->task_start, t->ntask, t->toff, t->soff, t->txy, t->sxy, t->su,
-                               t->near, t->nnear, t->centre + G.lvl_off[G.L], t->loc + G.lvl_off[G.L] * (G.p + 1),
-                               G.p, G.self_mode, t->tperm, phi, t->status);
+  static const bool use_ref = getenv("FMM_P2P_LIBDEVICE") && getenv("FMM_P2P_LIBDEVICE")[0] == '1';
+  if (use_ref) {  // A/B reference: libdevice log / atan2 (not the product path)
+    int blocks = 148 * 32;
+    k_p2p<<<blocks, 128, 0, s>>>(t->task_leaf, t->task_start, t->ntask, t->toff, t->soff, t->txy, t->sxy, t->su,
+                                 t->near, t->nnear, t->centre + G.lvl_off[G.L],
+                                 t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, G.self_mode, t->tperm, phi, t->status);
+  } else {
+    FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
+    int blocks = 148 * 8;  // persistent-style grid, tasks claimed dynamically
+    k_p2p_fast<<<blocks, 128, 0, s>>>(t->task_leaf, t->task_start, t->ntask, t->next_task, t->toff, t->soff, t->txy,
+                                      t->sxy, t->su, t->near, t->nnear, t->centre + G.lvl_off[G.L],
+                                      t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, G.self_mode, t->tperm, t->p2p_tab,
+                                      phi, t->status);
+  }
   t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s) {
+  k_debug_p2p_math<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const double2*)dxdy, n, tabs, (double2*)out);
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
