@@ -190,21 +190,30 @@ def run_gpu(args):
     clocks.start()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
     launches = 0
     p2p_ms, down_ms, up_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
+    kept = []  # trees stay alive until after the timed region (no host syncs inside it)
     for s in range(args.steps):
+        step_ev[s].record(stream)
         n_l, trees = one_step(timing=True)
         launches += n_l
+        kept.append(trees)
+    step_ev[args.steps].record(stream)
+    e1.record(stream)
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    log(f"[bench] per-step ms: {[round(x, 2) for x in step_ms]}")
+    for trees in kept:
         for nm, t in trees.items():
             ms = t.stage_times()
             up_ms[nm] += ms[3]
             down_ms[nm] += ms[4]
             p2p_ms[nm] += ms[5]
             t.close()
-    e1.record(stream)
-    barrier()
-    ms_total = e0.elapsed_time(e1)
+    kept.clear()
     clk = clocks.stop(local)
     ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:

@@ -60,8 +60,9 @@ extern "C" {
  * p       : expansion terms, 1..31 (multipole Q, a_1..a_p; local b_0..b_p).
  * self_mode: 1 when targets are the sources; the pair (i, i) is skipped by index (D16).
  * rank / nranks: target-leaf partition for multi-GPU runs;
- *                single GPU: 0 / 1.  Rank r evaluates the targets of leaf range
- *                [K*r/nranks, K*(r+1)/nranks) of its work-balanced split; see fmm_rank_range. */
+ *                single GPU: 0 / 1.  Every rank gets the full input; rank r evaluates
+ *                the targets of its work-balanced leaf range (fmm_partition,
+ *                fmm_rank_range). */
 typedef struct {
   int32_t tiling;
   int32_t depth;
@@ -146,6 +147,21 @@ int fmm_stage_times(fmm_tree_t t, float* ms6);
 /* Leaf range [lo, hi) of target leaves evaluated by cfg->rank (balanced by the
  * estimated near-field work; requires a built tree for the counts). */
 int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi);
+
+/* Work-balanced split of the target leaves for multi-GPU runs (host function; used by
+ * fmm_build_tree when cfg->nranks > 1, exported for tests).  block_work[b] is the
+ * estimated evaluation work of leaves [b*leaves_per_block, (b+1)*leaves_per_block);
+ * rank r gets the leaf range [*lo, *hi) between the block boundaries whose prefix work
+ * is closest to r*W/nranks and (r+1)*W/nranks.  Ranges of ranks 0..nranks-1 are
+ * contiguous, disjoint and cover [0, K). */
+int fmm_partition(const double* block_work, int64_t nblocks, int64_t leaves_per_block, int64_t K, int32_t rank,
+                  int32_t nranks, int64_t* lo, int64_t* hi);
+
+/* Grow the device's default stream-ordered memory pool by allocating and releasing
+ * `bytes` (trees allocate from it; the library sets its release threshold to infinity). */
+int fmm_pool_reserve(size_t bytes);
+/* Device bytes held by a tree's slab. */
+size_t fmm_tree_bytes(fmm_tree_t t);
 
 /* Number of this library's kernel launches enqueued by the last build / evaluate. */
 int64_t fmm_launch_count(fmm_tree_t t);

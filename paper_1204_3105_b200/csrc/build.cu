@@ -427,6 +427,63 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   return FMM_OK;
 }
 
+namespace {
+// estimated evaluation work of each leaf (P2P pairs + per-target L2P + per-leaf downward),
+// summed over blocks of FMM_PART_BLOCK leaves (the multi-rank partition)
+__global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int p,
+                             double* __restrict__ bw) {
+  __shared__ double warp_sum[FMM_PART_BLOCK / 32];
+  int64_t leaf = blockIdx.x * (int64_t)FMM_PART_BLOCK + threadIdx.x;
+  double w = 0.0;
+  if (leaf < K) {
+    int nt = toff[leaf + 1] - toff[leaf];
+    if (nt > 0) {
+      int64_t ns = 0;
+      for (int q = 0; q < nnear[leaf]; ++q) {
+        int sl = near[leaf * FMM_NEAR_MAX + q];
+        ns += soff[sl + 1] - soff[sl];
+      }
+      w = (double)nt * (double)ns + 2.0 * (p + 1) * nt + 40.0 * (p + 1) * (p + 1);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < FMM_PART_BLOCK / 32; ++i) s += warp_sum[i];
+    bw[blockIdx.x] = s;
+  }
+}
+}  // namespace
+
+// near lists of every leaf; for nranks > 1 the work-balanced leaf range of this rank
+int fmm_stage_near_partition(fmm_tree_s* t) {
+  cudaStream_t s = t->stream;
+  const Geo& G = t->g;
+  DGeo g = dgeo(G);
+  k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->soff, t->toff, t->near, t->nnear, 0, G.K);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
+  if (t->cfg.nranks <= 1) {
+    t->leaf_lo = 0;
+    t->leaf_hi = G.K;
+    return FMM_OK;
+  }
+  int64_t nb = (G.K + FMM_PART_BLOCK - 1) / FMM_PART_BLOCK;
+  double* bw = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&bw, nb * sizeof(double), s));
+  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->soff, t->toff, t->near, t->nnear, G.p, bw);
+  t->launches++;
+  std::vector<double> hb(nb);
+  cudaError_t ce = cudaMemcpyAsync(hb.data(), bw, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  cudaFreeAsync(bw, s);
+  FMM_CUDA_TRY(ce);
+  return fmm_partition(hb.data(), nb, FMM_PART_BLOCK, G.K, t->cfg.rank, t->cfg.nranks, &t->leaf_lo, &t->leaf_hi);
+}
+
 int fmm_stage_tables_lists(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
@@ -435,16 +492,13 @@ int fmm_stage_tables_lists(fmm_tree_s* t) {
     k_centres<<<blocks_for(G.ncells[l], 256), 256, 0, s>>>(g, l, G.ncells[l], t->centre + G.lvl_off[l]);
     t->launches++;
   }
+  int e = fmm_stage_near_partition(t);
+  if (e) return e;
   for (int l = 1; l <= G.L; ++l) {
     int64_t np = G.ncells[l - 1];
     k_lists_level<<<blocks_for(np, 128), 128, 0, s>>>(g, l, t->soff, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
                                                       t->ncand + G.lvl_off[l - 1], t->e4mask + G.lvl_off[l],
                                                       t->leaf_lo, t->leaf_hi);
-    t->launches++;
-  }
-  int64_t nl = t->leaf_hi - t->leaf_lo;
-  if (nl > 0) {
-    k_near<<<blocks_for(nl, 128), 128, 0, s>>>(g, t->soff, t->toff, t->near, t->nnear, t->leaf_lo, t->leaf_hi);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());

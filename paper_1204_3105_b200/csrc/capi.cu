@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI of include/fmm_b200.h: configuration checks, device memory
 // (one stream-ordered slab per tree), host<->device staging, stage sequencing, exports.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -101,6 +102,7 @@ int make_geo(const fmm_config* c, Geo* g) {
   g->p = c->p;
   g->self_mode = c->self_mode ? 1 : 0;
   g->K = ipow64(g->B, g->L);
+  g->nslot = g->tiling == FMM_QUADTREE ? 9 : (g->tiling == FMM_SEPTREE ? 7 : 13);
   g->lvl_off[0] = 0;
   for (int l = 0; l <= g->L; ++l) {
     g->ncells[l] = ipow64(g->B, l);
@@ -166,9 +168,10 @@ void carve(fmm_tree_s* t, Arena& a) {
   t->e4mask = a.take<unsigned long long>(G.total_cells);
   t->near = a.take<int32_t>(K * FMM_NEAR_MAX);
   t->nnear = a.take<int32_t>(K);
-  t->ntask_cap = m / 32 + (t->leaf_hi - t->leaf_lo) + 1;
-  t->task_leaf = a.take<int32_t>(t->ntask_cap);
-  t->task_start = a.take<int32_t>(t->ntask_cap);
+  // every (leaf, near leaf) block gives at most ceil(rows / 8) tasks
+  t->ntask_cap = (int64_t)G.nslot * (m / 8 + G.K) + 1;
+  t->tasks = a.take<int4>(t->ntask_cap);
+  t->part = a.take<double2>((m + 1) * (int64_t)G.nslot);
   t->ntask = a.take<int32_t>(1);
   t->next_task = a.take<int32_t>(1);
   t->p2p_tab = a.take<double>(P2P_TAB_DOUBLES);
@@ -189,6 +192,19 @@ int free_tree(fmm_tree_s* t) {
   for (int i = 0; i < 8; ++i)
     if (t->ev[i]) cudaEventDestroy(t->ev[i]);
   delete t;
+  return FMM_OK;
+}
+
+// FMM_DEBUG_SYNC=1: synchronise after every stage and name the stage of a CUDA fault
+int debug_sync(cudaStream_t s, const char* stage) {
+  static const bool on = getenv("FMM_DEBUG_SYNC") && getenv("FMM_DEBUG_SYNC")[0] == '1';
+  if (!on) return FMM_OK;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fmm_set_error_message(std::string("stage ") + stage + ": " + cudaGetErrorString(e));
+    return FMM_ECUDA;
+  }
   return FMM_OK;
 }
 
@@ -214,6 +230,46 @@ int stage_input(fmm_tree_s* t, const double* src, size_t bytes, int slot, const 
 extern "C" {
 
 int fmm_version(void) { return 1; }
+
+int fmm_partition(const double* block_work, int64_t nblocks, int64_t leaves_per_block, int64_t K, int32_t rank,
+                  int32_t nranks, int64_t* lo, int64_t* hi) {
+  if (!lo || !hi || nranks < 1 || rank < 0 || rank >= nranks || nblocks < 0 || leaves_per_block < 1 || K < 0 ||
+      (nblocks > 0 && !block_work))
+    return FMM_EBADCFG;
+  double W = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) W += block_work[b] > 0.0 ? block_work[b] : 0.0;
+  // cut(r): the block boundary whose prefix work is closest to r W / nranks (monotone in r)
+  auto cut = [&](int32_t r) -> int64_t {
+    if (r <= 0) return 0;
+    if (r >= nranks) return nblocks;
+    double target = W * (double)r / (double)nranks, pre = 0.0;
+    int64_t b = 0;
+    while (b < nblocks && pre + (block_work[b] > 0.0 ? block_work[b] : 0.0) <= target) {
+      pre += block_work[b] > 0.0 ? block_work[b] : 0.0;
+      ++b;
+    }
+    if (b < nblocks) {
+      double next = pre + (block_work[b] > 0.0 ? block_work[b] : 0.0);
+      if (next - target < target - pre) ++b;
+    }
+    return b;
+  };
+  int64_t c0 = cut(rank), c1 = cut(rank + 1);
+  *lo = std::min(c0 * leaves_per_block, K);
+  *hi = std::min(c1 * leaves_per_block, K);
+  return FMM_OK;
+}
+
+int fmm_pool_reserve(size_t bytes) {
+  init_pool_once();
+  void* p = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync(&p, bytes, 0));
+  FMM_CUDA_TRY(cudaFreeAsync(p, 0));
+  FMM_CUDA_TRY(cudaStreamSynchronize(0));
+  return FMM_OK;
+}
+
+size_t fmm_tree_bytes(fmm_tree_t t) { return t ? t->slab_bytes : 0; }
 
 const char* fmm_error_string(int code) {
   switch (code) {
@@ -251,8 +307,8 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   t->stream = (cudaStream_t)stream;
   t->n = n;
   t->m = m;
-  t->leaf_lo = g.K * cfg->rank / cfg->nranks;
-  t->leaf_hi = g.K * (cfg->rank + 1) / cfg->nranks;
+  t->leaf_lo = 0;  // the rank's range is set by fmm_stage_near_partition
+  t->leaf_hi = g.K;
   cudaStream_t s = t->stream;
   // inputs
   e = stage_input(t, src_xy, (size_t)n * 16, 0, &t->src_xy_in);
@@ -276,6 +332,7 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   a.base = slab;
   carve(t, a);
   t->slab = slab;
+  t->slab_bytes = sizer.off;
   static std::vector<double> hb = host_binom();
   static std::vector<double> htab = [] {
     std::vector<double> v(P2P_TAB_DOUBLES);
@@ -292,8 +349,11 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
     return FMM_ECUDA;
   }
   e = fmm_stage_keys_sort(t);
+  if (!e) e = debug_sync(s, "keys+sort");
   if (!e) e = fmm_stage_tables_lists(t);
+  if (!e) e = debug_sync(s, "tables+lists");
   if (!e) e = fmm_build_tasks(t);
+  if (!e) e = debug_sync(s, "tasks");
   if (e) {
     free_tree(t);
     return e;
@@ -329,10 +389,13 @@ int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
   }
   if (t->timing) cudaEventRecord(t->ev[3], s);
   int e = fmm_stage_upward(t);
+  if (!e) e = debug_sync(s, "upward");
   if (t->timing) cudaEventRecord(t->ev[4], s);
   if (!e) e = fmm_stage_downward(t);
+  if (!e) e = debug_sync(s, "downward");
   if (t->timing) cudaEventRecord(t->ev[5], s);
   if (!e) e = fmm_stage_p2p(t, phi);
+  if (!e) e = debug_sync(s, "p2p");
   if (t->timing) cudaEventRecord(t->ev[6], s);
   if (!e && !dev) FMM_CUDA_TRY(cudaMemcpyAsync(phi_out, tmp, (size_t)t->m * 16, cudaMemcpyDeviceToHost, s));
   if (tmp) cudaFreeAsync(tmp, s);

@@ -13,10 +13,12 @@
 #define FMM_MAX_P 32
 #define FMM_CAND_MAX 64  // >= 4*13 (triangle), 7*7 (septree), 4*9 (quad) E4 candidates per sibling group
 #define FMM_NEAR_MAX 16  // >= 13 (triangle near set incl. self)
+#define FMM_PART_BLOCK 256  // leaves per work block of the multi-rank partition
 
 // ---------------------------------------------------------------- host-side geometry constants
 struct Geo {
   int tiling, L, B, p, self_mode;
+  int nslot;              // max near-list length (partial-sum slots per target)
   int64_t K;              // B^L leaves
   int64_t ncells[17];     // B^l
   int64_t lvl_off[18];    // start of level l in the all-level cell arrays
@@ -62,8 +64,8 @@ struct fmm_tree_s {
   int32_t* near;   // [K][FMM_NEAR_MAX]
   int32_t* nnear;  // [K]
   // P2P work list
-  int32_t* task_leaf;  // [ntask_cap]
-  int32_t* task_start; // [ntask_cap] sorted target position of the chunk start
+  int4* tasks;         // [ntask_cap] (leaf t, q | q_rev << 8 | flags, row0, row1) of p2p.cu
+  double2* part;       // [m][nslot] per (target, near-leaf) partial sums (Re, Im) of the near field
   int32_t* ntask;      // [1] device counter
   int32_t* next_task;  // [1] dynamic scheduling counter of the P2P kernel
   int64_t ntask_cap;
@@ -82,6 +84,7 @@ struct fmm_tree_s {
   float stage_ms[6];
   int64_t launches;
   void* slab;  // single allocation holding every tree buffer
+  size_t slab_bytes;
   // scratch for sort
   void* scratch;
   size_t scratch_bytes;
@@ -101,6 +104,7 @@ void fmm_set_error_message(const std::string& s);
 // ---------------------------------------------------------------- stage entry points (host)
 // build.cu
 int fmm_stage_keys_sort(fmm_tree_s* t);
+int fmm_stage_near_partition(fmm_tree_s* t);
 int fmm_stage_tables_lists(fmm_tree_s* t);
 int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
                         cudaStream_t s, int64_t* launches);

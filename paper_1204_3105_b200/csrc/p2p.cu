@@ -1,0 +1,312 @@
+// p2p.cu -- the near field, Phi_near(y_j) = sum over near leaves of sum_i u_i Log(y_j - x_i)
+// (SURVEY §8(a) a11), fused with L2P of the leaf locals and the
+// store at the caller's index (a10, a12).
+//
+// Work unit = one (target leaf t, near leaf s) block.  In self mode (targets = sources,
+// reading D16) the near relation is symmetric, and so is the kernel up to the branch of
+// Arg: Log(x_i - x_j) = Log(x_j - x_i) +/- i pi, with the same log|z|^2.  A light
+// off-diagonal block (t < s) is therefore evaluated ONCE: every pair feeds the row
+// target (u_j Log(x_i - x_j)) and, reversed, the column target (u_i Log(x_j - x_i)).
+// Diagonal blocks, heavy blocks (split by rows) and the distinct-target configs use
+// one-sided blocks.  Every (target, near-leaf) pair of the near list owns one partial-sum
+// slot written by exactly one task in a fixed order, and a final pass adds the slots in
+// near-list order, so the result is deterministic.
+#include "fmm_internal.cuh"
+#include "p2p_math.cuh"
+
+namespace {
+
+constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) block
+constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17;
+
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// rows per one-sided task of a block with ns sources (a multiple of 8, >= 8)
+__device__ __forceinline__ int split_rows(int ns) { return max(8, (P2P_LIGHT / max(ns, 1)) & ~7); }
+
+// tasks of target leaf t: count (out == nullptr) or write them from *pos
+__device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
+                          const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int self_mode,
+                          int64_t lo, int64_t hi, int4* out) {
+  const int nt = toff[t + 1] - toff[t];
+  if (nt == 0) return 0;
+  const bool t_in = t >= lo && t < hi;
+  const int nn = nnear[t];
+  int c = 0;
+  auto emit_rows = [&](int leaf, int qq, int rows, int ns, int flags) {
+    const int rs = split_rows(ns);
+    for (int r0 = 0; r0 < rows; r0 += rs) {
+      if (out) out[c] = make_int4(leaf, qq | flags, r0, min(rows, r0 + rs));
+      ++c;
+    }
+  };
+  for (int q = 0; q < nn; ++q) {
+    const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
+    const int ns = soff[s + 1] - soff[s];
+    if (!self_mode) {
+      if (t_in) emit_rows(t, q, nt, ns, 0);
+      continue;
+    }
+    if (s < t) continue;  // the block belongs to the smaller leaf index
+    if (s == t) {
+      if (t_in) emit_rows(t, q, nt, ns, TF_DIAG);
+      continue;
+    }
+    const bool s_in = s >= lo && s < hi;
+    // index of t in near(s)
+    int qr = 0;
+    for (int k = 0; k < nnear[s]; ++k)
+      if (near[(int64_t)s * FMM_NEAR_MAX + k] == t) qr = k;
+    if ((int64_t)nt * ns <= P2P_LIGHT) {
+      if (t_in || s_in) {
+        if (out) out[c] = make_int4(t, q | (qr << 8) | TF_SYM, 0, nt);
+        ++c;
+      }
+    } else {
+      if (t_in) emit_rows(t, q, nt, ns, 0);
+      if (s_in) emit_rows(s, qr, ns, nt, 0);
+    }
+  }
+  return c;
+}
+
+__global__ void k_task_count(int64_t K, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
+                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int self_mode,
+                             int64_t lo, int64_t hi, int32_t* __restrict__ cnt) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > K) return;
+  cnt[t] = t < K ? leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, nullptr) : 0;
+}
+
+__global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
+                            const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int self_mode,
+                            int64_t lo, int64_t hi, const int32_t* __restrict__ start, int4* __restrict__ tasks,
+                            int32_t* __restrict__ ntask) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > K) return;
+  if (t == K) {
+    *ntask = start[K];
+    return;
+  }
+  leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, tasks + start[t]);
+}
+
+// ------------------------------------------------------------------ the pair kernel
+// Lane = (phase, row): row = lane % 8 (8 target rows of the block), phase = lane / 8 (4 source
+// columns per step).  Sources of s are staged 32 at a time in shared memory.
+__global__ void __launch_bounds__(128, 6) k_p2p_pairs(
+    const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
+    const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
+    const double2* __restrict__ sxy, const double* __restrict__ su, const int32_t* __restrict__ near,
+    const int32_t* __restrict__ tperm, const double* __restrict__ tabs, double2* __restrict__ part, int nslot,
+    int64_t lo, int64_t hi, DevStatus* st) {
+  __shared__ double2 s_log[P2P_LOG_N];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  __shared__ double2 s_xy[4][32];
+  __shared__ double s_u[4][32];
+  p2p_load_tables(tabs, s_log, s_atan);
+  const uint32_t a_log = (uint32_t)__cvta_generic_to_shared(s_log);
+  const uint32_t a_atan = (uint32_t)__cvta_generic_to_shared(s_atan);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tl = lane & 7, phase = lane >> 3;
+  const double PI = 3.141592653589793;
+  const int ntask = *ntask_p;
+  while (true) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(next_task, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= ntask) break;
+    const int4 tk = tasks[task];
+    const int t = tk.x, q = tk.y & 0xff, qr = (tk.y >> 8) & 0xff;
+    const bool sym = tk.y & TF_SYM, diag = tk.y & TF_DIAG;
+    const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
+    const int tb = toff[t], sb = soff[s], ns = soff[s + 1] - sb;
+    const bool write_rows = t >= lo && t < hi;
+    const bool write_react = sym && s >= lo && s < hi;
+    for (int rc = tk.z; rc < tk.w; rc += 8) {
+      const int row = rc + tl;
+      const bool rvalid = row < tk.w;
+      const double2 y = rvalid ? txy[tb + row] : make_double2(1.0e5, 1.0e5);
+      const double urow = (sym && rvalid) ? su[tb + row] : 0.0;  // self mode: the row target is also a source
+      double acc_k = 0.0, acc_z = 0.0, acc_i = 0.0;
+      for (int c0 = 0; c0 < ns; c0 += 32) {
+        if (c0 + lane < ns) {
+          s_xy[w][lane] = sxy[sb + c0 + lane];
+          s_u[w][lane] = su[sb + c0 + lane];
+        }
+        __syncwarp();
+        const int cnt = min(32, ns - c0);
+        double R_re = 0.0, R_im = 0.0;  // reaction on column 4 * tl + phase of this chunk
+#pragma unroll 2
+        for (int it = 0; it < 8; ++it) {
+          const int k = 4 * it + phase;
+          const bool valid = k < cnt && rvalid;
+          const double2 x = s_xy[w][k];
+          const double uc = valid ? s_u[w][k] : 0.0;
+          double dx = y.x - x.x, dy = y.y - x.y;
+          // excluded pair (i, i) of a diagonal block (D16) and padding: z := 1 + 0i gives
+          // log|z|^2 = 0 and Arg z = 0 exactly
+          if (!valid || (diag && c0 + k == row)) {
+            dx = 1.0;
+            dy = 0.0;
+          }
+          const double r2 = fma(dx, dx, dy * dy);
+          double kd, lz, ag;
+          if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
+            kd = 0.0;
+            if (r2 == 0.0) {
+              unsigned long long bad = tperm[tb + row];
+              if (sym) bad = min(bad, (unsigned long long)tperm[sb + c0 + k]);
+              atomicMin(&st->coincident_bad, bad);
+              lz = 0.0;
+              ag = 0.0;
+            } else {
+              lz = 2.0 * log(hypot(dx, dy));
+              ag = atan2(__dadd_rn(dy, 0.0), dx);
+            }
+          } else {
+            p2p_log_split(r2, a_log, &kd, &lz);
+            ag = p2p_atan2(dy, dx, a_atan);
+          }
+          acc_k = fma(uc, kd, acc_k);
+          acc_z = fma(uc, lz, acc_z);
+          acc_i = fma(uc, ag, acc_i);
+          if (sym) {
+            // reversed pair: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
+            double v_re = urow * fma(kd, P2P_C[10], lz);
+            double v_im = urow * (ag > 0.0 ? ag - PI : ag + PI);
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+              v_re += __shfl_xor_sync(0xffffffffu, v_re, o);
+              v_im += __shfl_xor_sync(0xffffffffu, v_im, o);
+            }
+            if (tl == it) {
+              R_re += v_re;
+              R_im += v_im;
+            }
+          }
+        }
+        if (write_react) {
+          const int k = 4 * tl + phase;
+          if (k < cnt) {
+            double2* slot = part + ((int64_t)(sb + c0 + k) * nslot + qr);
+            if (rc == tk.z) {
+              *slot = make_double2(R_re, R_im);
+            } else {
+              const double2 o = *slot;
+              *slot = make_double2(o.x + R_re, o.y + R_im);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // reduce the 4 phases of each row (lanes tl, tl+8, tl+16, tl+24)
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1) {
+        acc_k += __shfl_xor_sync(0xffffffffu, acc_k, o);
+        acc_z += __shfl_xor_sync(0xffffffffu, acc_z, o);
+        acc_i += __shfl_xor_sync(0xffffffffu, acc_i, o);
+      }
+      if (phase == 0 && rvalid && write_rows) {
+        const double re = fma(acc_k, P2P_C[10], acc_z) + acc_k * P2P_C[11];  // + ln 2 * sum u k
+        part[(int64_t)(tb + row) * nslot + q] = make_double2(re, acc_i);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ partial sums + L2P -> Phi
+// one warp per target leaf; lanes over its targets; slots added in near-list order
+__global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, const int32_t* __restrict__ toff,
+                                                    const int32_t* __restrict__ nnear, const double2* __restrict__ txy,
+                                                    const double2* __restrict__ cen_leaf,
+                                                    const double2* __restrict__ loc_leaf, int p,
+                                                    const int32_t* __restrict__ tperm,
+                                                    const double2* __restrict__ part, int nslot,
+                                                    double2* __restrict__ phi) {
+  const int64_t t = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= hi) return;
+  const int tb = toff[t], nt = toff[t + 1] - tb;
+  if (nt == 0) return;
+  const int nn = nnear[t];
+  const double2 c = cen_leaf[t];
+  const double2* b = loc_leaf + t * (p + 1);
+  for (int i = lane; i < nt; i += 32) {
+    const int tpos = tb + i;
+    double re = 0.0, im = 0.0;
+    for (int q = 0; q < nn; ++q) {
+      const double2 v = part[(int64_t)tpos * nslot + q];
+      re += v.x;
+      im += v.y;
+    }
+    const double2 y = txy[tpos];
+    const double2 z = make_double2(y.x - c.x, y.y - c.y);
+    double2 acc = b[p];  // L2P by Horner at y - c_leaf
+    for (int k = p - 1; k >= 0; --k) {
+      acc = cmul2(acc, z);
+      acc.x += b[k].x;
+      acc.y += b[k].y;
+    }
+    phi[tperm[tpos]] = make_double2(acc.x + 0.5 * re, acc.y + im);
+  }
+}
+
+// debug hook: the P2P math on explicit (dx, dy) pairs -> (log |z|^2, Arg z)
+__global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
+                                 double2* __restrict__ out) {
+  __shared__ double2 s_log[P2P_LOG_N];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  p2p_load_tables(tabs, s_log, s_atan);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double dx = d[i].x, dy = d[i].y;
+  double r2 = fma(dx, dx, dy * dy);
+  out[i] = make_double2(p2p_log(r2, (uint32_t)__cvta_generic_to_shared(s_log)),
+                        p2p_atan2(dy, dx, (uint32_t)__cvta_generic_to_shared(s_atan)));
+}
+
+}  // namespace
+
+int fmm_build_tasks(fmm_tree_s* t) {
+  cudaStream_t s = t->stream;
+  const int64_t K = t->g.K;
+  int32_t* cnt = nullptr;
+  size_t sb = fmm_scan_scratch_bytes(K + 1);
+  FMM_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (K + 1) + sb, s));
+  k_task_count<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear,
+                                                                t->g.self_mode, t->leaf_lo, t->leaf_hi, cnt);
+  int e = fmm_device_scan_i32(cnt, cnt, K + 1, cnt + K + 1, sb, s, &t->launches);
+  if (!e)
+    k_task_fill<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear,
+                                                                 t->g.self_mode, t->leaf_lo, t->leaf_hi, cnt,
+                                                                 t->tasks, t->ntask);
+  t->launches += 2;
+  cudaFreeAsync(cnt, s);
+  FMM_CUDA_TRY(cudaGetLastError());
+  return e;
+}
+
+int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
+  const Geo& G = t->g;
+  cudaStream_t s = t->stream;
+  FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
+  k_p2p_pairs<<<148 * 6, 128, 0, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
+                                       t->near, t->tperm, t->p2p_tab, t->part, G.nslot, t->leaf_lo, t->leaf_hi, t->status);
+  const int64_t nl = t->leaf_hi - t->leaf_lo;
+  if (nl > 0)
+    k_p2p_finish<<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(
+        t->leaf_lo, t->leaf_hi, t->toff, t->nnear, t->txy, t->centre + G.lvl_off[G.L],
+        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, G.nslot, phi);
+  t->launches += 2;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s) {
+  k_debug_p2p_math<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const double2*)dxdy, n, tabs, (double2*)out);
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}

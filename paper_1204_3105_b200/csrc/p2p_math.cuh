@@ -19,6 +19,8 @@
 #include <stdint.h>
 
 #define P2P_LOG_N 128
+#define P2P_TW 8  // targets per P2P warp task
+#define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
 #define P2P_ATAN_K 32  // t_k = k / 32, k = 0..32
 // table layout (doubles): [0, 256) log (1/c, log c) pairs; [256, 256 + 2*8*33) (T[oct][k], t_k)
 #define P2P_TAB_LOG 0
@@ -67,6 +69,15 @@ __device__ __forceinline__ float p2p_rcpf(float x) {
   return r;
 }
 
+// |x| as binary32 by truncation of the binary64 pattern (exponent rebias with a clamp at 0)
+__device__ __forceinline__ float p2p_d2f_trunc(double x) {
+  int h = __double2hiint(x) & 0x7fffffff;
+  int lo = __double2loint(x);
+  int e = max((h >> 20) - (1023 - 127), 0);  // binary32 biased exponent (0 -> ~0)
+  int m = ((h & 0xfffff) << 3) | ((unsigned)lo >> 29);
+  return __int_as_float(e > 0 ? ((e << 23) | m) : 0);
+}
+
 // log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
 // The 128 intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
@@ -79,11 +90,13 @@ __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double
   double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
-  double q = fma(r, P2P_C[0], P2P_C[1]);
-  q = fma(q, r, P2P_C[2]);
-  q = fma(q, r, P2P_C[3]);
-  q = fma(q, r, P2P_C[4]);
-  q = fma(q, r, P2P_C[5]);
+  // r^5..r^7 coefficients rounded to 20-bit mantissas (SASS immediates): their error
+  // (< 2^-21 relative) times r^n/n stays below 2^-60 for |r| <= 2^-8
+  double q = fma(r, 0x1.2492400000000p-3 /* ~1/7 */, -0x1.5555500000000p-3 /* ~-1/6 */);
+  q = fma(q, r, 0x1.9999900000000p-3 /* ~1/5 */);
+  q = fma(q, r, -0.25);
+  q = fma(q, r, P2P_C[4]);  // 1/3 (full precision)
+  q = fma(q, r, -0.5);
   *lz = cl.y + fma(r_2, q, r);  // log c_i + log1p(r)
   *kd = (double)k;
 }
@@ -96,7 +109,8 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 
 // Arg(dx + i dy) in (-pi, pi], a zero imaginary part read as +0 (D13); |z| >= 1e-30
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
-  // FP32 estimate of t = min/max of |dx|, |dy| (both representable: |z| >= 1e-30)
+  // FP32 estimate of t = min/max of |dx|, |dy| (|z| >= 1e-30 keeps the larger one a normal
+  // binary32; a smaller one that flushes to 0 only means t ~ 0)
   float fx = fabsf(__double2float_rn(dx)), fy = fabsf(__double2float_rn(dy));
   bool swap = fy > fx;
   float tf = fminf(fx, fy) * p2p_rcpf(fmaxf(fx, fy));
@@ -113,9 +127,10 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   double b = fma(Tt.y, num, den);
   double q = a * p2p_rcp(b);
   double q2 = q * q;
-  double P = fma(q2, P2P_C[6], P2P_C[7]);
-  P = fma(P, q2, P2P_C[8]);
-  P = fma(P, q2, P2P_C[9]);
+  // q^7, q^9 coefficients rounded to 20-bit mantissas (immediates), error < 2^-60 |q|
+  double P = fma(q2, 0x1.c71c700000000p-4 /* ~1/9 */, -0x1.2492400000000p-3 /* ~-1/7 */);
+  P = fma(P, q2, P2P_C[8]);  // 1/5
+  P = fma(P, q2, P2P_C[9]);  // -1/3
   double at = fma(q * q2, P, q);
   // sign S = (-1)^(swap + dxneg + dyneg) applied by flipping the sign bit
   int par = ((int)swap ^ (int)dyneg ^ (hx >> 31)) & 1;

@@ -110,265 +110,110 @@ __global__ void __launch_bounds__(128) k_m2m(int B, int64_t nparents, int64_t sp
   }
 }
 
-// ------------------------------------------------------------------ downward: L2L + M2L (one warp per target cell)
-__global__ void __launch_bounds__(128) k_down(int l, int B, int64_t ncells, int64_t span_l,
-                                              const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
-                                              const double2* __restrict__ cen_l, const double2* __restrict__ cen_par,
-                                              const double2* __restrict__ loc_par, const int32_t* __restrict__ cand,
-                                              const int32_t* __restrict__ ncand,
-                                              const unsigned long long* __restrict__ e4mask,
-                                              const double2* __restrict__ mp_l, int p,
-                                              const double* __restrict__ binom, double2* __restrict__ loc_l) {
-  __shared__ double2 at_s[4][32];
-  int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
+// ------------------------------------------------------------------ downward v2 (templated on P >= p)
+// One warp per target cell t with targets; lane l owns local coefficient b_l.
+//  * L2L from the parent (l >= 2): Horner in w = c_t - c_par over k = p..l.
+//  * M2L over E4(t) in batches of 16 sources.  Phase A (lane j = source j): w_j = 1/(c_s - c_t),
+//    all powers w_j^k -> shared memory, Log(c_t - c_s) (D13 iii) and Q_j.  Phase B, per source:
+//    lane l forms a~_l = (-1)^l a_l w^l (Pascal-scaled form), then
+//    b_l += w^l (sum_k C(l+k-1, k-1) a~_k - Q/l) with its binomial row C(l+k-1, k-1) held in
+//    registers; lane 0 adds Q Log(c_t - c_s) + sum_k a~_k.
+template <int P>
+__global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int64_t span_l,
+                                               const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
+                                               const double2* __restrict__ cen_l, const double2* __restrict__ cen_par,
+                                               const double2* __restrict__ loc_par, const int32_t* __restrict__ cand,
+                                               const unsigned long long* __restrict__ e4mask,
+                                               const double2* __restrict__ mp_l, int p,
+                                               const double* __restrict__ binom, double2* __restrict__ loc_l) {
+  constexpr int NB = 16;  // sources per batch
+  __shared__ double2 s_pw[4][NB][P + 1];
+  __shared__ double2 s_lg[4][NB];
+  __shared__ double s_q[4][NB];
+  __shared__ double2 s_at[4][32];
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
   if (t >= ncells) return;
-  int64_t tl = max(t * span_l, leaf_lo), th = min((t + 1) * span_l, leaf_hi);
-  if (th <= tl || toff[th] == toff[tl]) return;  // no targets of this rank below t
-  double2 ct = cen_l[t];
+  const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
+  if (thi <= tlo || toff[thi] == toff[tlo]) return;  // no targets of this rank below t
+  const double2 ct = cen_l[t];
   double2 acc = make_double2(0.0, 0.0);
-  const int L_ = lane;  // output coefficient handled by this lane (p <= 31)
+  const bool out_lane = lane <= p;
+  // binomial row of this lane: C(l+k-1, k-1), k = 1..P (0 beyond p)
+  double cb[P];
+#pragma unroll
+  for (int k = 1; k <= P; ++k) cb[k - 1] = (k <= p && out_lane) ? binom[(lane + k - 1) * BS + (k - 1)] : 0.0;
+  const double inv_l = lane > 0 ? 1.0 / lane : 0.0;
+  const int64_t par = t / B;
   if (l >= 2) {
-    int64_t par = t / B;
-    double2 cpp = cen_par[par];
-    double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
+    const double2 cpp = cen_par[par];
+    const double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
     const double2* bp = loc_par + par * (p + 1);
     for (int k = p; k >= 0; --k) {
-      double2 bk = bp[k];
-      if (k >= L_ && L_ <= p) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + L_], bk));
+      const double2 bk = bp[k];
+      if (k >= lane && out_lane) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + lane], bk));
     }
   }
-  int64_t par = t / B;
   unsigned long long mask = e4mask[t];
   const int32_t* cd = cand + par * FMM_CAND_MAX;
   while (mask) {
-    int i = __ffsll((long long)mask) - 1;
-    mask &= mask - 1;
-    int64_t s = cd[i];
-    double2 cs = cen_l[s];
-    double2 z0 = make_double2(cs.x - ct.x, cs.y - ct.y);
-    double2 wv = cinv(z0);
-    // w^lane by an inclusive product scan (lane 0 holds 1)
-    double2 pw = lane == 0 ? make_double2(1.0, 0.0) : wv;
+    // ---- phase A: up to NB sources, lane j handles source j
+    int nb = 0;
+    int src_j = -1;
+    {
+      unsigned long long mm = mask;
+      for (int j = 0; j < NB && mm; ++j) {
+        int i = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        if (lane == j) src_j = cd[i];
+        ++nb;
+      }
+      mask = mm;
+    }
+    if (lane < nb) {
+      const double2 cs = cen_l[src_j];
+      const double zx = cs.x - ct.x, zy = cs.y - ct.y;
+      const double d = 1.0 / (zx * zx + zy * zy);
+      const double2 wv = make_double2(zx * d, -zy * d);
+      double2 pw = make_double2(1.0, 0.0);
+      s_pw[w][lane][0] = pw;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      double2 y = make_double2(__shfl_up_sync(0xffffffffu, pw.x, o), __shfl_up_sync(0xffffffffu, pw.y, o));
-      if (lane >= o) pw = cmul(pw, y);
-    }
-    const double2* a = mp_l + s * (p + 1);
-    double2 ak = (lane <= p) ? a[lane] : make_double2(0.0, 0.0);
-    double Q = __shfl_sync(0xffffffffu, ak.x, 0);
-    double2 at = cmul(ak, pw);
-    if (lane & 1) at = make_double2(-at.x, -at.y);
-    at_s[w][lane] = at;
-    __syncwarp();
-    double2 sum = make_double2(0.0, 0.0);
-    if (L_ <= p) {
-      for (int k = 1; k <= p; ++k) sum = cadd(sum, cscale(binom[(L_ + k - 1) * BS + (k - 1)], at_s[w][k]));
-      if (L_ == 0) {
-        double2 lg = clog_principal(ct.x - cs.x, ct.y - cs.y);  // Log(c_L - c_M), D13 (iii)
-        acc = cadd(acc, cadd(cscale(Q, lg), sum));
-      } else {
-        acc = cadd(acc, cmul(pw, make_double2(sum.x - Q / L_, sum.y)));
+      for (int k = 1; k <= P; ++k) {
+        pw = cmul(pw, wv);
+        s_pw[w][lane][k] = pw;
       }
+      s_lg[w][lane] = clog_principal(ct.x - cs.x, ct.y - cs.y);  // Log(c_L - c_M), D13 (iii)
+      s_q[w][lane] = mp_l[(int64_t)src_j * (p + 1)].x;
     }
     __syncwarp();
-  }
-  if (L_ <= p) loc_l[t * (p + 1) + L_] = acc;
-}
-
-// ------------------------------------------------------------------ P2P task list
-__global__ void k_chunk_counts(const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
-                               int32_t* __restrict__ cnt) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t n = leaf_hi - leaf_lo;
-  if (i > n) return;
-  if (i == n) {
-    cnt[i] = 0;
-    return;
-  }
-  int64_t t = leaf_lo + i;
-  int nt = toff[t + 1] - toff[t];
-  cnt[i] = (nt + 31) / 32;
-}
-__global__ void k_fill_tasks(const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
-                             const int32_t* __restrict__ start, int32_t* __restrict__ task_leaf,
-                             int32_t* __restrict__ task_start, int32_t* ntask) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t n = leaf_hi - leaf_lo;
-  if (i >= n) return;
-  int64_t t = leaf_lo + i;
-  int nt = toff[t + 1] - toff[t];
-  int c = (nt + 31) / 32, s = start[i];
-  for (int k = 0; k < c; ++k) {
-    task_leaf[s + k] = (int32_t)t;
-    task_start[s + k] = toff[t] + 32 * k;
-  }
-  if (i == n - 1) *ntask = s + c;
-}
-
-// ------------------------------------------------------------------ L2P + P2P (one warp per 32-target chunk)
-// Sources of each near leaf are staged 32 at a time in shared memory (one coalesced load
-// per lane) and read back as broadcasts; log|z|^2 and Arg z come from p2p_math.cuh.
-// Tasks are claimed dynamically (one atomic per warp task) for load balance.
-__global__ void __launch_bounds__(128) k_p2p_fast(
-    const int32_t* __restrict__ task_leaf, const int32_t* __restrict__ task_start, const int32_t* __restrict__ ntask_p,
-    int32_t* __restrict__ next_task, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
-    const double2* __restrict__ txy, const double2* __restrict__ sxy, const double* __restrict__ su,
-    const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, const double2* __restrict__ cen_leaf,
-    const double2* __restrict__ loc_leaf, int p, int self_mode, const int32_t* __restrict__ tperm,
-    const double* __restrict__ tabs, double2* __restrict__ phi, DevStatus* st) {
-  __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
-  __shared__ double2 s_xy[4][32];
-  __shared__ double s_u[4][32];
-  p2p_load_tables(tabs, s_log, s_atan);
-  const uint32_t a_log = (uint32_t)__cvta_generic_to_shared(s_log);
-  const uint32_t a_atan = (uint32_t)__cvta_generic_to_shared(s_atan);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ntask = *ntask_p;
-  while (true) {
-    int task = 0;
-    if (lane == 0) task = atomicAdd(next_task, 1);
-    task = __shfl_sync(0xffffffffu, task, 0);
-    if (task >= ntask) break;
-    const int t = task_leaf[task];
-    const int tpos0 = task_start[task];
-    const int nt = min(32, toff[t + 1] - tpos0);
-    const int tpos = tpos0 + lane;
-    const bool active = lane < nt;
-    const double2 y = active ? txy[tpos] : make_double2(1.0e5, 1.0e5);
-    double re = 0.0, re_k = 0.0, im = 0.0;
-    const int nn = nnear[t];
-    for (int qn = 0; qn < nn; ++qn) {
-      const int sl = near[(int64_t)t * FMM_NEAR_MAX + qn];
-      const int s0 = soff[sl], s1 = soff[sl + 1];
-      for (int j0 = s0; j0 < s1; j0 += 32) {
-        const int j = j0 + lane;
-        if (j < s1) {
-          s_xy[w][lane] = sxy[j];
-          s_u[w][lane] = su[j];
-        }
-        __syncwarp();
-        const int cnt = min(32, s1 - j0);
-        const int excl = (self_mode && sl == t) ? (tpos - j0) : -1;
-#pragma unroll 2
-        for (int k = 0; k < cnt; ++k) {
-          const double2 x = s_xy[w][k];
-          const double uu = s_u[w][k];
-          double dx = y.x - x.x, dy = y.y - x.y;
-          // the pair (i, i) in self mode (D16): dx = dy = 0 exactly; z := 1 + 0i gives
-          // log|z|^2 = 0 and Arg z = 0 exactly, so the pair contributes nothing
-          if (k == excl) dx = 1.0;
-          const double r2 = fma(dx, dx, dy * dy);
-          double kd, lz, ag;
-          if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
-            kd = 0.0;
-            if (r2 == 0.0) {
-              if (active) atomicMin(&st->coincident_bad, (unsigned long long)tperm[tpos]);
-              lz = 0.0;
-              ag = 0.0;
-            } else {
-              lz = 2.0 * log(hypot(dx, dy));
-              ag = atan2(__dadd_rn(dy, 0.0), dx);
-            }
-          } else {
-            p2p_log_split(r2, a_log, &kd, &lz);
-            ag = p2p_atan2(dy, dx, a_atan);
-          }
-          re_k = fma(uu, kd, re_k);  // sum u k  (times ln 2 at the end)
-          re = fma(uu, lz, re);
-          im = fma(uu, ag, im);
-        }
-        __syncwarp();
+    // ---- phase B
+    for (int j = 0; j < nb; ++j) {
+      const int s = __shfl_sync(0xffffffffu, src_j, j);
+      const double2 a = out_lane ? mp_l[(int64_t)s * (p + 1) + lane] : make_double2(0.0, 0.0);
+      const double2 pwl = lane <= P ? s_pw[w][j][min(lane, P)] : make_double2(0.0, 0.0);
+      double2 at = cmul(a, pwl);
+      if (lane & 1) at = make_double2(-at.x, -at.y);
+      s_at[w][lane] = at;
+      __syncwarp();
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int k = 1; k <= (P < 32 ? P : 31); ++k) {  // p <= 31: coefficient 32 never exists
+        const double2 ak = s_at[w][k];
+        sr = fma(cb[k - 1], ak.x, sr);
+        si = fma(cb[k - 1], ak.y, si);
       }
-    }
-    if (active) {
-      const double2 c = cen_leaf[t];
-      const double2 z = make_double2(y.x - c.x, y.y - c.y);
-      const double2* b = loc_leaf + (int64_t)t * (p + 1);
-      double2 acc = b[p];
-      for (int k = p - 1; k >= 0; --k) acc = cadd(cmul(acc, z), b[k]);
-      re = fma(re_k, P2P_C[10], re) + re_k * P2P_C[11];  // + ln 2 * sum u k
-      phi[tperm[tpos]] = make_double2(acc.x + 0.5 * re, acc.y + im);
-    }
-  }
-}
-
-// debug hook: the P2P math on explicit (dx, dy) pairs -> (log |z|^2, Arg z)
-__global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
-                                 double2* __restrict__ out) {
-  __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
-  p2p_load_tables(tabs, s_log, s_atan);
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double dx = d[i].x, dy = d[i].y;
-  double r2 = fma(dx, dx, dy * dy);
-  out[i] = make_double2(p2p_log(r2, (uint32_t)__cvta_generic_to_shared(s_log)),
-                        p2p_atan2(dy, dx, (uint32_t)__cvta_generic_to_shared(s_atan)));
-}
-
-__global__ void __launch_bounds__(128) k_p2p(const int32_t* __restrict__ task_leaf, const int32_t* __restrict__ task_start,
-                                             const int32_t* __restrict__ ntask_p, const int32_t* __restrict__ toff,
-                                             const int32_t* __restrict__ soff, const double2* __restrict__ txy,
-                                             const double2* __restrict__ sxy, const double* __restrict__ su,
-                                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear,
-                                             const double2* __restrict__ cen_leaf, const double2* __restrict__ loc_leaf,
-                                             int p, int self_mode, const int32_t* __restrict__ tperm,
-                                             double2* __restrict__ phi, DevStatus* st) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int ntask = *ntask_p;
-  for (int64_t task = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; task < ntask; task += nwarps) {
-    int t = task_leaf[task];
-    int tpos0 = task_start[task];
-    int nt = min(32, toff[t + 1] - tpos0);
-    int tpos = tpos0 + lane;
-    bool active = lane < nt;
-    double2 y = active ? txy[tpos] : make_double2(0.0, 0.0);
-    double re = 0.0, im = 0.0;
-    int nn = nnear[t];
-    for (int q = 0; q < nn; ++q) {
-      int sl = near[(int64_t)t * FMM_NEAR_MAX + q];
-      int s0 = soff[sl], s1 = soff[sl + 1];
-      for (int j0 = s0; j0 < s1; j0 += 32) {
-        int j = j0 + lane;
-        double2 xs = j < s1 ? sxy[j] : make_double2(0.0, 0.0);
-        double us = j < s1 ? su[j] : 0.0;
-        int cnt = min(32, s1 - j0);
-        for (int k = 0; k < cnt; ++k) {
-          double xx = __shfl_sync(0xffffffffu, xs.x, k);
-          double xy = __shfl_sync(0xffffffffu, xs.y, k);
-          double uu = __shfl_sync(0xffffffffu, us, k);
-          double dx = y.x - xx, dy = __dadd_rn(y.y - xy, 0.0);
-          bool skip = !active || (self_mode && j0 + k == tpos);
-          double r2 = dx * dx + dy * dy;
-          if (!skip && r2 == 0.0) {
-            atomicMin(&st->coincident_bad, (unsigned long long)tperm[tpos]);
-            skip = true;
-          }
-          if (skip) {
-            dx = 1.0;
-            dy = 0.0;
-            r2 = 1.0;
-            uu = 0.0;
-          }
-          re += uu * log(r2);
-          im += uu * atan2(dy, dx);
-        }
+      const double Q = s_q[w][j];
+      if (lane == 0) {
+        const double2 lg = s_lg[w][j];
+        acc.x += Q * lg.x + sr;
+        acc.y += Q * lg.y + si;
+      } else if (out_lane) {
+        acc = cadd(acc, cmul(pwl, make_double2(fma(-Q, inv_l, sr), si)));
       }
-    }
-    if (active) {
-      // L2P by Horner at y - c_leaf
-      double2 c = cen_leaf[t];
-      double2 z = make_double2(y.x - c.x, y.y - c.y);
-      const double2* b = loc_leaf + (int64_t)t * (p + 1);
-      double2 acc = b[p];
-      for (int k = p - 1; k >= 0; --k) acc = cadd(cmul(acc, z), b[k]);
-      phi[tperm[tpos]] = make_double2(acc.x + 0.5 * re, acc.y + im);
+      __syncwarp();
     }
   }
+  if (out_lane) loc_l[t * (p + 1) + lane] = acc;
 }
 
 template <int P>
@@ -404,68 +249,31 @@ int fmm_stage_upward(fmm_tree_s* t) {
   return FMM_OK;
 }
 
+template <int P>
+static void launch_down(fmm_tree_s* t, int l) {
+  const Geo& G = t->g;
+  const int p = G.p;
+  const int64_t nc = G.ncells[l];
+  k_down2<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
+      l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
+      t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
+      t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
+}
+
 int fmm_stage_downward(fmm_tree_s* t) {
   const Geo& G = t->g;
-  cudaStream_t s = t->stream;
-  int p = G.p;
+  const int p = G.p;
   for (int l = 1; l <= G.L; ++l) {
-    int64_t nc = G.ncells[l];
-    const double2* cen_par = t->centre + G.lvl_off[l - 1];
-    const double2* loc_par = t->loc + G.lvl_off[l - 1] * (p + 1);
-    k_down<<<(unsigned)((nc * 32 + 127) / 128), 128, 0, s>>>(
-        l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
-        cen_par, loc_par, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX, t->ncand + G.lvl_off[l - 1],
-        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
+    if (p <= 8) launch_down<8>(t, l);
+    else if (p <= 12) launch_down<12>(t, l);
+    else if (p <= 16) launch_down<16>(t, l);
+    else if (p <= 20) launch_down<20>(t, l);
+    else if (p <= 24) launch_down<24>(t, l);
+    else if (p <= 28) launch_down<28>(t, l);
+    else launch_down<32>(t, l);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
 
-int fmm_build_tasks(fmm_tree_s* t) {
-  cudaStream_t s = t->stream;
-  int64_t nl = t->leaf_hi - t->leaf_lo;
-  FMM_CUDA_TRY(cudaMemsetAsync(t->ntask, 0, sizeof(int32_t), s));
-  if (nl <= 0) return FMM_OK;
-  int32_t* cnt = nullptr;
-  size_t sb = fmm_scan_scratch_bytes(nl + 1);
-  FMM_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (nl + 1) + sb, s));
-  k_chunk_counts<<<(unsigned)((nl + 1 + 255) / 256), 256, 0, s>>>(t->toff, t->leaf_lo, t->leaf_hi, cnt);
-  int e = fmm_device_scan_i32(cnt, cnt, nl + 1, cnt + nl + 1, sb, s, &t->launches);
-  if (!e) {
-    k_fill_tasks<<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t->toff, t->leaf_lo, t->leaf_hi, cnt, t->task_leaf,
-                                                              t->task_start, t->ntask);
-  }
-  t->launches += 2;
-  cudaFreeAsync(cnt, s);
-  FMM_CUDA_TRY(cudaGetLastError());
-  return e;
-}
-
-int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
-  const Geo& G = t->g;
-  cudaStream_t s = t->stream;
-  static const bool use_ref = getenv("FMM_P2P_LIBDEVICE") && getenv("FMM_P2P_LIBDEVICE")[0] == '1';
-  if (use_ref) {  // A/B reference: libdevice log / atan2 (not the product path)
-    int blocks = 148 * 32;
-    k_p2p<<<blocks, 128, 0, s>>>(t->task_leaf, t->task_start, t->ntask, t->toff, t->soff, t->txy, t->sxy, t->su,
-                                 t->near, t->nnear, t->centre + G.lvl_off[G.L],
-                                 t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, G.self_mode, t->tperm, phi, t->status);
-  } else {
-    FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
-    int blocks = 148 * 8;  // persistent-style grid, tasks claimed dynamically
-    k_p2p_fast<<<blocks, 128, 0, s>>>(t->task_leaf, t->task_start, t->ntask, t->next_task, t->toff, t->soff, t->txy,
-                                      t->sxy, t->su, t->near, t->nnear, t->centre + G.lvl_off[G.L],
-                                      t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, G.self_mode, t->tperm, t->p2p_tab,
-                                      phi, t->status);
-  }
-  t->launches++;
-  FMM_CUDA_TRY(cudaGetLastError());
-  return FMM_OK;
-}
-
-int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s) {
-  k_debug_p2p_math<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const double2*)dxdy, n, tabs, (double2*)out);
-  FMM_CUDA_TRY(cudaGetLastError());
-  return FMM_OK;
-}
