@@ -138,58 +138,77 @@ __global__ void __launch_bounds__(128, 6) k_p2p_pairs(
         }
         __syncwarp();
         const int cnt = min(32, ns - c0);
-        double R_re = 0.0, R_im = 0.0;  // reaction on column 4 * tl + phase of this chunk
-#pragma unroll 2
-        for (int it = 0; it < 8; ++it) {
-          const int k = 4 * it + phase;
-          const bool valid = k < cnt && rvalid;
-          const double2 x = s_xy[w][k];
-          const double uc = valid ? s_u[w][k] : 0.0;
-          double dx = y.x - x.x, dy = y.y - x.y;
-          // excluded pair (i, i) of a diagonal block (D16) and padding: z := 1 + 0i gives
-          // log|z|^2 = 0 and Arg z = 0 exactly
-          if (!valid || (diag && c0 + k == row)) {
-            dx = 1.0;
-            dy = 0.0;
-          }
-          const double r2 = fma(dx, dx, dy * dy);
-          double kd, lz, ag;
-          if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
-            kd = 0.0;
-            if (r2 == 0.0) {
-              unsigned long long bad = tperm[tb + row];
-              if (sym) bad = min(bad, (unsigned long long)tperm[sb + c0 + k]);
-              atomicMin(&st->coincident_bad, bad);
-              lz = 0.0;
-              ag = 0.0;
-            } else {
-              lz = 2.0 * log(hypot(dx, dy));
-              ag = atan2(__dadd_rn(dy, 0.0), dx);
-            }
-          } else {
-            p2p_log_split(r2, a_log, &kd, &lz);
-            ag = p2p_atan2(dy, dx, a_atan);
-          }
-          acc_k = fma(uc, kd, acc_k);
-          acc_z = fma(uc, lz, acc_z);
-          acc_i = fma(uc, ag, acc_i);
-          if (sym) {
-            // reversed pair: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
-            double v_re = urow * fma(kd, P2P_C[10], lz);
-            double v_im = urow * (ag > 0.0 ? ag - PI : ag + PI);
+        // reaction on this lane's column of the chunk, k_own = 4 * (4 * b0 + 2 * b2 + b1) + phase
+        // (tl = b2 b1 b0): see the reduce-scatter below
+        double R_re = 0.0, R_im = 0.0;
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
-              v_re += __shfl_xor_sync(0xffffffffu, v_re, o);
-              v_im += __shfl_xor_sync(0xffffffffu, v_im, o);
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
+          double vr[4], vi[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = 4 * (4 * h + j) + phase;
+            const bool valid = k < cnt && rvalid;
+            const double2 x = s_xy[w][k];
+            const double uc = valid ? s_u[w][k] : 0.0;
+            double dx = y.x - x.x, dy = y.y - x.y;
+            // excluded pair (i, i) of a diagonal block (D16) and padding: z := 1 + 0i gives
+            // log|z|^2 = 0 and Arg z = 0 exactly
+            if (!valid || (diag && c0 + k == row)) {
+              dx = 1.0;
+              dy = 0.0;
             }
-            if (tl == it) {
-              R_re += v_re;
-              R_im += v_im;
+            const double r2 = fma(dx, dx, dy * dy);
+            double kd, lz, ag;
+            if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
+              kd = 0.0;
+              if (r2 == 0.0) {
+                unsigned long long bad = tperm[tb + row];
+                if (sym) bad = min(bad, (unsigned long long)tperm[sb + c0 + k]);
+                atomicMin(&st->coincident_bad, bad);
+                lz = 0.0;
+                ag = 0.0;
+              } else {
+                lz = 2.0 * log(hypot(dx, dy));
+                ag = atan2(__dadd_rn(dy, 0.0), dx);
+              }
+            } else {
+              p2p_log_split(r2, a_log, &kd, &lz);
+              ag = p2p_atan2(dy, dx, a_atan);
+            }
+            acc_k = fma(uc, kd, acc_k);
+            acc_z = fma(uc, lz, acc_z);
+            acc_i = fma(uc, ag, acc_i);
+            // reversed pair: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
+            vr[j] = urow * fma(kd, P2P_C[10], lz);
+            vi[j] = urow * (ag > 0.0 ? ag - PI : ag + PI);
+          }
+          if (sym) {
+            // reduce-scatter over the 8 row lanes (tl) of this phase: halving xor 4, 2, then
+            // the xor-1 pair adds; lane (b2 b1 b0) ends with column j = 2 b2 + b1 of group h
+            const bool b2 = tl & 4, b1 = tl & 2, b0 = tl & 1;
+            double s0r = b2 ? vr[0] : vr[2], s0i = b2 ? vi[0] : vi[2];
+            double s1r = b2 ? vr[1] : vr[3], s1i = b2 ? vi[1] : vi[3];
+            double k0r = b2 ? vr[2] : vr[0], k0i = b2 ? vi[2] : vi[0];
+            double k1r = b2 ? vr[3] : vr[1], k1i = b2 ? vi[3] : vi[1];
+            k0r += __shfl_xor_sync(0xffffffffu, s0r, 4);
+            k0i += __shfl_xor_sync(0xffffffffu, s0i, 4);
+            k1r += __shfl_xor_sync(0xffffffffu, s1r, 4);
+            k1i += __shfl_xor_sync(0xffffffffu, s1i, 4);
+            double sr = b1 ? k0r : k1r, si = b1 ? k0i : k1i;
+            double mr = b1 ? k1r : k0r, mi = b1 ? k1i : k0i;
+            mr += __shfl_xor_sync(0xffffffffu, sr, 2);
+            mi += __shfl_xor_sync(0xffffffffu, si, 2);
+            mr += __shfl_xor_sync(0xffffffffu, mr, 1);
+            mi += __shfl_xor_sync(0xffffffffu, mi, 1);
+            if ((int)b0 == h) {
+              R_re = mr;
+              R_im = mi;
             }
           }
         }
         if (write_react) {
-          const int k = 4 * tl + phase;
+          const int k = 4 * (4 * (tl & 1) + 2 * ((tl >> 2) & 1) + ((tl >> 1) & 1)) + phase;
           if (k < cnt) {
             double2* slot = part + ((int64_t)(sb + c0 + k) * nslot + qr);
             if (rc == tk.z) {
