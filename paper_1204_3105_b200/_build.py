@@ -34,32 +34,37 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile every csrc/*.cu into `out` (default: the in-tree libfmm_b200.so).  `defines`
+    (e.g. ["P2P_MINB=4"]) are tuning knobs for building variants to compare on the GPU."""
+    target = out or SO
+    if not force and not defines and out is None and up_to_date():
         return SO
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objs = []
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
     logs = []
     for src in sources():
-        obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
+        obj = os.path.join(PKG, "build", os.path.basename(src) + tag + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
         objs.append(obj)
-    tmp = SO + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, SO)
-    with open(os.path.join(PKG, "build", "ptxas.log"), "w") as f:
+    os.replace(tmp, target)
+    with open(os.path.join(PKG, "build", "ptxas" + (tag if defines else "") + ".log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return SO
+    return target
 
 
 if __name__ == "__main__":

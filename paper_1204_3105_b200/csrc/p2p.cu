@@ -96,7 +96,10 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 // ------------------------------------------------------------------ the pair kernel
 // Lane = (phase, row): row = lane % 8 (8 target rows of the block), phase = lane / 8 (4 source
 // columns per step).  Sources of s are staged 32 at a time in shared memory.
-__global__ void __launch_bounds__(128, 6) k_p2p_pairs(
+#ifndef P2P_MINB
+#define P2P_MINB 6  // resident blocks per SM the register allocation is sized for
+#endif
+__global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
     const double2* __restrict__ sxy, const double* __restrict__ su, const int32_t* __restrict__ near,

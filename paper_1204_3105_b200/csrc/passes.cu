@@ -36,19 +36,21 @@ __device__ __forceinline__ double2 clog_principal(double dx, double dy) {
 }
 
 // ------------------------------------------------------------------ P2M (one warp per leaf)
+// 8 lanes per leaf (4 leaves per warp): each lane accumulates u z^k over every 8th source of
+// its leaf, then a 3-step xor reduction within the 8-lane group.
 template <int P>
 __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, const double* __restrict__ su,
                                              const int32_t* __restrict__ soff, const double2* __restrict__ cen,
                                              int64_t K, int p, double2* __restrict__ mp) {
-  int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (leaf >= K) return;
-  int s0 = soff[leaf], s1 = soff[leaf + 1];
-  double2 c = cen[leaf];
+  const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool lvalid = leaf < K;
+  const int s0 = lvalid ? soff[leaf] : 0, s1 = lvalid ? soff[leaf + 1] : 0;
+  const double2 c = lvalid ? cen[leaf] : make_double2(0.0, 0.0);
   double Sr[P + 1], Si[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) Sr[k] = Si[k] = 0.0;
-  for (int i = s0 + lane; i < s1; i += 32) {
+  for (int i = s0 + sub; i < s1; i += 8) {
     double2 x = sxy[i];
     double u = su[i];
     double zr = x.x - c.x, zi = x.y - c.y;
@@ -66,15 +68,16 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 1; o < 8; o <<= 1) {
       Sr[k] += __shfl_xor_sync(0xffffffffu, Sr[k], o);
       Si[k] += __shfl_xor_sync(0xffffffffu, Si[k], o);
     }
   }
+  if (!lvalid) return;
   double2* out = mp + leaf * (p + 1);
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
-    if (k <= p && lane == (k & 31)) {
+    if (k <= p && sub == (k & 7)) {
       out[k] = (k == 0) ? make_double2(Sr[0], 0.0) : make_double2(-Sr[k] / k, -Si[k] / k);
     }
   }
@@ -219,8 +222,7 @@ __global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int
 template <int P>
 void launch_p2m(fmm_tree_s* t) {
   const Geo& G = t->g;
-  int64_t warps = G.K;
-  k_p2m<P><<<(unsigned)((warps * 32 + 127) / 128), 128, 0, t->stream>>>(
+  k_p2m<P><<<(unsigned)((G.K * 8 + 127) / 128), 128, 0, t->stream>>>(
       t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], G.K, G.p, t->mp + G.lvl_off[G.L] * (G.p + 1));
 }
 
