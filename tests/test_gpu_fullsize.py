@@ -1,0 +1,101 @@
+"""GPU parity at BASELINE.json's full sizes (-m gpu), in the launch configuration bench.py
+times (device-resident inputs, fmm_build_tree + fmm_evaluate on the default stream).
+
+Bit-exact over EVERY point / cell: leaf keys, the sort permutation, leaf CSR offsets,
+cell centres of every level, near and E4 lists of every level.  Potentials: the oracle
+FMM evaluated one by one on a seeded sample of 1024 targets plus every target of the most
+loaded leaf (normwise <= 1e-12, D15), and, on a smaller sample, both within the paper's
+truncation bound of the direct sum (Re only, D13/D14)."""
+import numpy as np
+import pytest
+
+import fmm_inputs as fi
+from gpu_common import gpu_tree, normwise, oracle_tree
+
+pytestmark = pytest.mark.gpu
+
+FULL = ["C3", "C4q", "C4s", "C4t", "C5"]
+
+
+@pytest.fixture(scope="module")
+def cache():
+    return {}
+
+
+def setup(cache, name):
+    if name not in cache:
+        cache.clear()  # one full-size config in memory at a time
+        w = fi.get(name)
+        d = fi.generate(w)
+        g = gpu_tree(w, d)
+        phi = g.evaluate().cpu().numpy()
+        g.check()
+        o = oracle_tree(w, d)
+        cache[name] = (w, d, g, o, phi)
+    return cache[name]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_fullsize_tree_bit_exact(cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = setup(cache, name)
+    sk, tk = o.keys()
+    assert np.array_equal(g.export(X.SRC_KEYS), sk)
+    sp, tp = o.perm()
+    assert np.array_equal(g.export(X.SRC_PERM), sp)
+    so, to = o.leaf_offsets()
+    assert np.array_equal(g.export(X.SRC_OFFSETS), so)
+    if not w.self_mode:
+        assert np.array_equal(g.export(X.TGT_KEYS), tk)
+        assert np.array_equal(g.export(X.TGT_PERM), tp)
+        assert np.array_equal(g.export(X.TGT_OFFSETS), to)
+    for l in range(w.depth + 1):
+        gc = g.export(X.CENTRES, l).reshape(-1, 2)
+        assert np.array_equal(gc.view(np.uint64), o.centres(l).view(np.uint64)), l
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_fullsize_lists_bit_exact(cache, name):
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = setup(cache, name)
+    ow, of, en = o.near_csr()
+    assert np.array_equal(g.export(X.NEAR_OWNERS), ow)
+    assert np.array_equal(g.export(X.NEAR_OFFSETS), of)
+    assert np.array_equal(g.export(X.NEAR_ENTRIES), en)
+    for l in range(1, w.depth + 1):
+        ow, of, en = o.e4_csr(l)
+        assert np.array_equal(g.export(X.E4_OWNERS, l), ow), l
+        assert np.array_equal(g.export(X.E4_OFFSETS, l), of), l
+        assert np.array_equal(g.export(X.E4_ENTRIES, l), en), l
+
+
+def sample_ids(w, o, seed=5):
+    rng = np.random.default_rng(seed)
+    ids = rng.choice(w.m, size=1024, replace=False)
+    _, to = o.leaf_offsets()
+    counts = np.diff(to)
+    heavy = int(np.argmax(counts))
+    _, tperm = o.perm()
+    heavy_ids = tperm[to[heavy]:to[heavy + 1]]
+    return np.unique(np.concatenate([ids, heavy_ids]).astype(np.int64))
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_fullsize_potentials_sampled(cache, name):
+    w, d, g, o, phi = setup(cache, name)
+    ids = sample_ids(w, o)
+    ref = o.evaluate(ids)
+    assert normwise(phi[ids], ref) <= 1e-12
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_fullsize_within_paper_bound_of_direct_sum(cache, name):
+    import oracle
+
+    w, d, g, o, phi = setup(cache, name)
+    ids = sample_ids(w, o)[:48]
+    direct = oracle.direct(d["src_xy"], d["u"], d["tgt_xy"], w.self_mode, ids)
+    bound = o.bound(ids)
+    assert np.all(np.abs(phi[ids].real - direct.real) <= bound)
