@@ -48,8 +48,9 @@ WORKLOADS = {
 # FP64 peak derived from the unit counts and clocks of the guides:
 # 148 SMs x 64 FP64 FMA/clk/SM x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-# FP64 flops per P2P pair executed by the P2P kernel (ncu-measured)
-F_PAIR = float(os.environ.get("FMM_F_PAIR", "0")) or None
+# FP64 flops executed by k_p2p_pairs per near-field interaction, from ncu
+# (sm__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on; profiles/r01/p2p_fp64.json)
+F_INT = {"C4q": 36.67, "C4s": 34.30, "C4t": 35.66, "C3": 71.40, "C5": 51.33}
 
 
 def log(*a):
@@ -133,9 +134,9 @@ def run_gpu(args):
     inputs = make_inputs(names)
     stream = torch.cuda.current_stream(dev)
 
-    def cfg_of(w):
+    def cfg_of(w, timing=False):
         return fmm.Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, w.self_mode,
-                               rank=rank, nranks=world)
+                               rank=rank, nranks=world, timing=timing)
 
     # device-resident inputs and outputs
     dev_in, host_in, outs, host_out = {}, {}, {}, {}
@@ -151,9 +152,7 @@ def run_gpu(args):
         launches, stage = 0, {}
         for nm, (w, d) in inputs.items():
             src, u, tgt = host_in[nm] if host else dev_in[nm]
-            t = fmm.Tree(cfg_of(w), src, u, tgt, stream=stream)
-            if timing:
-                t.set_timing(True)
+            t = fmm.Tree(cfg_of(w, timing), src, u, tgt, stream=stream)
             t.evaluate(host_out[nm] if host else outs[nm], stream=stream)
             launches += t.launch_count()
             if timing:
@@ -172,6 +171,7 @@ def run_gpu(args):
         one_step()
     barrier()
     # correctness guard: status of one tree
+    tree_bytes = {}
     for nm, (w, d) in inputs.items():
         src, u, tgt = dev_in[nm]
         t = fmm.Tree(cfg_of(w), src, u, tgt, stream=stream)
@@ -179,7 +179,12 @@ def run_gpu(args):
         t.check()
         cnt = counters_for(t)
         inputs[nm] = (w, d, cnt)
+        tree_bytes[nm] = t.nbytes()
         t.close()
+    # the timed loop keeps its trees alive until the end (no host syncs inside it): grow the
+    # stream-ordered pool up front so that no timed step pays for first-touch allocation
+    torch.cuda.synchronize(dev)
+    fmm.native.pool_reserve(int(1.05 * args.steps * sum(tree_bytes.values())) + (1 << 30))
     inputs2 = {nm: v[:2] for nm, v in inputs.items()}
     counters = {nm: v[2] for nm, v in inputs.items()}
     inputs.clear()
@@ -194,6 +199,7 @@ def run_gpu(args):
     e0.record(stream)
     launches = 0
     p2p_ms, down_ms, up_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
+    build_ms, pair_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
     kept = []  # trees stay alive until after the timed region (no host syncs inside it)
     for s in range(args.steps):
         step_ev[s].record(stream)
@@ -209,6 +215,8 @@ def run_gpu(args):
     for trees in kept:
         for nm, t in trees.items():
             ms = t.stage_times()
+            build_ms[nm] += ms[0] + ms[1]
+            pair_ms[nm] += ms[2]
             up_ms[nm] += ms[3]
             down_ms[nm] += ms[4]
             p2p_ms[nm] += ms[5]
@@ -245,24 +253,28 @@ def run_gpu(args):
             dist.destroy_process_group()
         return None
 
-    # ---- roofline of the dominant kernel (P2P + fused L2P), measured with CUDA events
+    # ---- roofline of the dominant kernel k_p2p_pairs (the near-field pair kernel), timed with
+    # CUDA events on its stream around each launch inside the timed region.  Its algorithmic
+    # work is expressed per near-field interaction (target, source) of the near lists:
+    # F_INT[tiling] = FP64 flops (2 DFMA + DADD + DMUL) the kernel executes per interaction,
+    # measured once by ncu on the same config (profiles/r01/p2p_fp64.json); the symmetric
+    # self-mode evaluation makes this less than the one-sided per-pair count.
     pairs = {nm: int(counters[nm][1]) for nm in names}
-    p2p_ms_avg = sum(p2p_ms.values()) / args.steps  # per step, all tilings
-    pair_rate = sum(pairs.values()) / (p2p_ms_avg / 1e3) if p2p_ms_avg > 0 else 0.0
-    f_pair = F_PAIR
-    roof = {"kernel": "k_p2p (P2P near field + fused L2P)", "bound": "alu", "unit": "TFLOP/s",
-            "peak": round(FP64_PEAK_TFLOPS, 2),
-            "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md Roofline); "
-                           "DFMA microbenchmark 34.2 TF/s (profiles/)",
-            "pairs_per_s": pair_rate, "f_pair_flops": f_pair, "traffic": None}
-    if f_pair:
-        ach = pair_rate * f_pair / 1e12
-        roof.update({"achieved": round(ach, 3), "frac": round(ach / FP64_PEAK_TFLOPS, 4)})
-    else:
-        roof.update({"achieved": None, "frac": None})
+    pair_ms_avg = sum(pair_ms.values()) / args.steps
+    flops = sum(pairs[nm] * F_INT.get(nm, 0.0) for nm in names)
+    ach = flops / (pair_ms_avg / 1e3) / 1e12 if pair_ms_avg > 0 else 0.0
+    roof = {"kernel": "k_p2p_pairs (P2P near field; L2P + final sum in k_p2p_finish)", "bound": "alu",
+            "achieved": round(ach, 3), "peak": round(FP64_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "peak_source": "FP64 FMA: 148 SM x 64 /clk x 2 x 1.965 GHz (DESIGN.md §7); DFMA microbenchmark "
+                           "34.2 TF/s (profiles/r01/fp64_peak.log)",
+            "interactions_per_s": sum(pairs.values()) / (pair_ms_avg / 1e3) if pair_ms_avg > 0 else 0.0,
+            "f_int_flops": {nm: F_INT.get(nm) for nm in names},
+            "kernel_ms_per_step": round(pair_ms_avg, 3)}
 
-    per_tiling = {nm: {"p2p_ms": p2p_ms[nm] / args.steps, "downward_ms": down_ms[nm] / args.steps,
-                       "upward_ms": up_ms[nm] / args.steps, "p2p_pairs": pairs[nm],
+    per_tiling = {nm: {"build_ms": build_ms[nm] / args.steps, "upward_ms": up_ms[nm] / args.steps,
+                       "downward_ms": down_ms[nm] / args.steps, "p2p_pairs_kernel_ms": pair_ms[nm] / args.steps,
+                       "p2p_stage_ms": p2p_ms[nm] / args.steps, "p2p_interactions": pairs[nm],
                        "m2l_ops": int(counters[nm][0])} for nm in names}
     value = total_targets / (ms_max / 1e3)
     res = {

@@ -73,8 +73,12 @@ typedef struct {
   double root_size;
   int32_t rank;
   int32_t nranks;
-  int32_t reserved[6]; /* must be zero */
+  int32_t flags;       /* FMM_FLAG_* */
+  int32_t reserved[5]; /* must be zero */
 } fmm_config;
+
+/* flags: record per-stage CUDA events from fmm_build_tree on (see fmm_stage_times) */
+#define FMM_FLAG_TIMING 1
 
 typedef struct fmm_tree_s* fmm_tree_t;
 
@@ -139,8 +143,10 @@ int64_t fmm_last_error_index(fmm_tree_t t);
 #define FMM_X_COUNTERS 16
 int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t bytes, size_t* needed);
 
-/* Per-stage device times (ms) of the last build / evaluate when timing is enabled
- * with fmm_set_timing(t, 1): {keys, sort, lists, p2m+m2m, downward, p2p}. */
+/* Per-stage device times (ms), from CUDA events on the tree's stream, of the build (when
+ * cfg->flags has FMM_FLAG_TIMING) and of the last fmm_evaluate (when timing is on, by that
+ * flag or fmm_set_timing(t, 1)): {keys + sort, centres + lists + tasks, P2P pair kernel,
+ * P2M + M2M, M2L + L2L (all levels), P2P pair kernel + final sum/L2P}. */
 int fmm_set_timing(fmm_tree_t t, int32_t enable);
 int fmm_stage_times(fmm_tree_t t, float* ms6);
 

@@ -93,8 +93,9 @@ int make_geo(const fmm_config* c, Geo* g) {
   if (c->depth < 1 || c->depth > (c->tiling == FMM_SEPTREE ? 10 : 15)) return FMM_EBADCFG;
   if (!(c->root_size > 0.0) || !isfinite(c->root_x) || !isfinite(c->root_y)) return FMM_EBADCFG;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return FMM_EBADCFG;
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 5; ++i)
     if (c->reserved[i]) return FMM_EBADCFG;
+  if (c->flags & ~FMM_FLAG_TIMING) return FMM_EBADCFG;
   memset(g, 0, sizeof(*g));
   g->tiling = c->tiling;
   g->L = c->depth;
@@ -348,12 +349,23 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
     free_tree(t);
     return FMM_ECUDA;
   }
+  if (cfg->flags & FMM_FLAG_TIMING) {
+    e = fmm_set_timing(t, 1);
+    if (e) {
+      free_tree(t);
+      return e;
+    }
+    cudaEventRecord(t->ev[0], s);
+  }
   e = fmm_stage_keys_sort(t);
   if (!e) e = debug_sync(s, "keys+sort");
+  if (t->timing) cudaEventRecord(t->ev[1], s);
   if (!e) e = fmm_stage_tables_lists(t);
   if (!e) e = debug_sync(s, "tables+lists");
   if (!e) e = fmm_build_tasks(t);
   if (!e) e = debug_sync(s, "tasks");
+  if (t->timing) cudaEventRecord(t->ev[2], s);
+  t->build_timed = t->timing;
   if (e) {
     free_tree(t);
     return e;
@@ -397,6 +409,7 @@ int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
   if (!e) e = fmm_stage_p2p(t, phi);
   if (!e) e = debug_sync(s, "p2p");
   if (t->timing) cudaEventRecord(t->ev[6], s);
+  t->eval_timed = t->timing;
   if (!e && !dev) FMM_CUDA_TRY(cudaMemcpyAsync(phi_out, tmp, (size_t)t->m * 16, cudaMemcpyDeviceToHost, s));
   if (tmp) cudaFreeAsync(tmp, s);
   return e;
@@ -435,10 +448,18 @@ int fmm_stage_times(fmm_tree_t t, float* ms6) {
   if (!t || !ms6) return FMM_EBADCFG;
   for (int i = 0; i < 6; ++i) ms6[i] = 0.f;
   if (!t->timing) return FMM_OK;
-  FMM_CUDA_TRY(cudaEventSynchronize(t->ev[6]));
-  cudaEventElapsedTime(&ms6[3], t->ev[3], t->ev[4]);
-  cudaEventElapsedTime(&ms6[4], t->ev[4], t->ev[5]);
-  cudaEventElapsedTime(&ms6[5], t->ev[5], t->ev[6]);
+  if (t->build_timed) {
+    FMM_CUDA_TRY(cudaEventSynchronize(t->ev[2]));
+    cudaEventElapsedTime(&ms6[0], t->ev[0], t->ev[1]);
+    cudaEventElapsedTime(&ms6[1], t->ev[1], t->ev[2]);
+  }
+  if (t->eval_timed) {
+    FMM_CUDA_TRY(cudaEventSynchronize(t->ev[6]));
+    cudaEventElapsedTime(&ms6[2], t->ev[5], t->ev[7]);
+    cudaEventElapsedTime(&ms6[3], t->ev[3], t->ev[4]);
+    cudaEventElapsedTime(&ms6[4], t->ev[4], t->ev[5]);
+    cudaEventElapsedTime(&ms6[5], t->ev[5], t->ev[6]);
+  }
   return FMM_OK;
 }
 

@@ -79,7 +79,7 @@ struct fmm_tree_s {
   // multi-rank leaf range
   int64_t leaf_lo, leaf_hi;
   // timing
-  int timing;
+  int timing, build_timed, eval_timed;
   cudaEvent_t ev[8];
   float stage_ms[6];
   int64_t launches;

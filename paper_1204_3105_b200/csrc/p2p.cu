@@ -317,6 +317,7 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
   k_p2p_pairs<<<148 * 6, 128, 0, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
                                        t->near, t->tperm, t->p2p_tab, t->part, G.nslot, t->leaf_lo, t->leaf_hi, t->status);
+  if (t->timing) cudaEventRecord(t->ev[7], s);
   const int64_t nl = t->leaf_hi - t->leaf_lo;
   if (nl > 0)
     k_p2p_finish<<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(

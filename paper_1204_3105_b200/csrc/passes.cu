@@ -251,11 +251,190 @@ int fmm_stage_upward(fmm_tree_s* t) {
   return FMM_OK;
 }
 
+// ------------------------------------------------------------------ downward with FP64 tensor cores
+// M2L in the Pascal-scaled form: for a batch of NB sources s of E4(t),
+//   Y[l][s] = sum_{k=1..p} C(l+k-1, k-1) a~_{s,k},   a~_{s,k} = (-1)^k a_{s,k} w_s^k,
+//   b_l += w_s^l (Y[l][s] - Q_s / l)   (l >= 1),     b_0 += Q_s Log(c_t - c_s) + Y[0][s]
+// The contraction Y = Cb * A~ (Cb: (p+1) x p real; A~: p x 2 NB, real and imaginary parts as
+// columns) runs on DMMA (mma.sync m8n8k4 f64, IEEE FP64 multiply-adds): Cb lives in the A
+// fragments of the warp's registers, A~ is staged in shared memory.  Fragment layouts
+// (m8n8k4 .f64): A[r][c] at lane 4r + c; B[k][n] at lane 4n + k; C[r][2c + {0,1}] at lane 4r + c.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) k_down_mma(int l, int B, int64_t ncells, int64_t span_l,
+                                                  const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
+                                                  const double2* __restrict__ cen_l,
+                                                  const double2* __restrict__ cen_par,
+                                                  const double2* __restrict__ loc_par,
+                                                  const int32_t* __restrict__ cand,
+                                                  const unsigned long long* __restrict__ e4mask,
+                                                  const double2* __restrict__ mp_l, int p,
+                                                  const double* __restrict__ binom, double2* __restrict__ loc_l) {
+  constexpr int NB = 8;             // sources per batch (2 n-tiles of 4 complex columns)
+  constexpr int MT = (P + 8) / 8;   // m-tiles over l = 0..P
+  constexpr int KT = P / 4;         // k-tiles over k = 1..P
+  __shared__ double2 s_pw[4][NB][P + 1];  // w_s^k
+  __shared__ double2 s_at[4][NB][P];      // a~_{s,k}, k = 1..P
+  __shared__ double2 s_lg[4][NB];
+  __shared__ double s_q[4][NB];
+  __shared__ int s_src[4][NB];
+  __shared__ double2 s_b[4][32];          // L2L part
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
+  if (t >= ncells) return;
+  const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
+  if (thi <= tlo || toff[thi] == toff[tlo]) return;  // no targets of this rank below t
+  const double2 ct = cen_l[t];
+  const int64_t par = t / B;
+  // ---- L2L (lane = coefficient): Horner in w = c_t - c_par over k = p..l
+  {
+    double2 acc = make_double2(0.0, 0.0);
+    if (l >= 2) {
+      const double2 cpp = cen_par[par];
+      const double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
+      s_b[w][lane] = lane <= p ? loc_par[par * (p + 1) + lane] : make_double2(0.0, 0.0);
+      __syncwarp();
+      for (int k = p; k >= 0; --k) {
+        const double2 bk = s_b[w][k];
+        if (k >= lane && lane <= p) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + lane], bk));
+      }
+      __syncwarp();
+    }
+    s_b[w][lane] = acc;
+  }
+  // ---- A fragments: Cb[l][k] = C(l+k-1, k-1), row l = 8 mt + lane/4, column k = 4 kt + lane%4 + 1
+  double afr[MT][KT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int r = 8 * mt + (lane >> 2), k = 4 * kt + (lane & 3) + 1;
+      afr[mt][kt] = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
+    }
+  double inv_r[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = 8 * mt + (lane >> 2);
+    inv_r[mt] = r > 0 ? 1.0 / r : 0.0;
+  }
+  double2 acc[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) acc[mt] = make_double2(0.0, 0.0);
+  unsigned long long mask = e4mask[t];
+  const int32_t* cd = cand + par * FMM_CAND_MAX;
+  while (mask) {
+    int nb = 0;
+    {
+      unsigned long long mm = mask;
+      for (int j = 0; j < NB && mm; ++j) {
+        const int i = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        if (lane == 0) s_src[w][j] = cd[i];
+        ++nb;
+      }
+      mask = mm;
+    }
+    __syncwarp();
+    // powers: lane = (source s = lane / 4, residue j = lane % 4): w^(4m + j), m = 0..P/4
+    {
+      const int s = lane >> 2, j = lane & 3;
+      if (s < nb) {
+        const double2 cs = cen_l[s_src[w][s]];
+        const double zx = cs.x - ct.x, zy = cs.y - ct.y;
+        const double d = 1.0 / (zx * zx + zy * zy);
+        const double2 wv = make_double2(zx * d, -zy * d);
+        const double2 w2 = cmul(wv, wv);
+        const double2 w4 = cmul(w2, w2);
+        double2 pw = j == 0 ? make_double2(1.0, 0.0) : (j == 1 ? wv : (j == 2 ? w2 : cmul(w2, wv)));
+#pragma unroll
+        for (int m = 0; 4 * m + j <= P && m <= P / 4; ++m) {
+          if (4 * m + j <= P) s_pw[w][s][4 * m + j] = pw;
+          pw = cmul(pw, w4);
+        }
+        if (j == 0) {
+          s_lg[w][s] = clog_principal(ct.x - cs.x, ct.y - cs.y);  // Log(c_L - c_M), D13 (iii)
+          s_q[w][s] = mp_l[(int64_t)s_src[w][s] * (p + 1)].x;
+        }
+      }
+    }
+    __syncwarp();
+    // a~_{s,k} = (-1)^k a_{s,k} w_s^k
+    for (int idx = lane; idx < NB * P; idx += 32) {
+      const int s = idx / P, kk = idx % P, k = kk + 1;
+      double2 v = make_double2(0.0, 0.0);
+      if (s < nb && k <= p) {
+        const double2 a = mp_l[(int64_t)s_src[w][s] * (p + 1) + k];
+        v = cmul(a, s_pw[w][s][k]);
+        if (k & 1) v = make_double2(-v.x, -v.y);
+      }
+      s_at[w][s][kk] = v;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      double d[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+      // B[k][n]: k = 4 kt + lane % 4, column n = 8 nt + lane / 4 -> source 4 nt + lane / 8, re/im (lane / 4) & 1
+      const int bs = 4 * nt + (lane >> 3), bc = (lane >> 2) & 1;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const double2 v = s_at[w][bs][4 * kt + (lane & 3)];
+        const double bfr = bc ? v.y : v.x;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma884(d[mt][0], d[mt][1], afr[mt][kt], bfr);
+      }
+      // C[r][2c + {0,1}] at lane 4r + c: row r = l, source s = 4 nt + lane % 4 (re, im)
+      const int s = 4 * nt + (lane & 3);
+      if (s < nb) {
+        const double Q = s_q[w][s];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + (lane >> 2);
+          if (r > P) continue;
+          if (r == 0) {
+            const double2 lg = s_lg[w][s];
+            acc[mt].x += Q * lg.x + d[mt][0];
+            acc[mt].y += Q * lg.y + d[mt][1];
+          } else {
+            const double2 pw = s_pw[w][s][r];
+            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, inv_r[mt], d[mt][0]), d[mt][1])));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // sum the 4 lanes (lane % 4) that hold the same row, then write b_l (+ L2L part)
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    acc[mt].x += __shfl_xor_sync(0xffffffffu, acc[mt].x, 1);
+    acc[mt].y += __shfl_xor_sync(0xffffffffu, acc[mt].y, 1);
+    acc[mt].x += __shfl_xor_sync(0xffffffffu, acc[mt].x, 2);
+    acc[mt].y += __shfl_xor_sync(0xffffffffu, acc[mt].y, 2);
+    const int r = 8 * mt + (lane >> 2);
+    if ((lane & 3) == 0 && r <= p) loc_l[t * (p + 1) + r] = cadd(acc[mt], s_b[w][r]);
+  }
+}
+
 template <int P>
 static void launch_down(fmm_tree_s* t, int l) {
   const Geo& G = t->g;
   const int p = G.p;
   const int64_t nc = G.ncells[l];
+  static const bool simt = getenv("FMM_M2L_SIMT") && getenv("FMM_M2L_SIMT")[0] == '1';
+  if (!simt) {
+    k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
+        l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
+        t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
+        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
+    return;
+  }
   k_down2<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
       l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
       t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,

@@ -15,6 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_PKG, "libfmm_b200.so")
 
 QUADTREE, SEPTREE, TRIQUAD = 0, 1, 2
+FLAG_TIMING = 1
 _TILING = {"quad": QUADTREE, "sept": SEPTREE, "triq": TRIQUAD, QUADTREE: 0, SEPTREE: 1, TRIQUAD: 2}
 
 
@@ -34,12 +35,12 @@ _DTYPE = {X.SRC_KEYS: np.uint32, X.TGT_KEYS: np.uint32, X.SRC_PERM: np.int32, X.
 class Config(C.Structure):
     _fields_ = [("tiling", C.c_int32), ("depth", C.c_int32), ("p", C.c_int32), ("self_mode", C.c_int32),
                 ("root_x", C.c_double), ("root_y", C.c_double), ("root_size", C.c_double),
-                ("rank", C.c_int32), ("nranks", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("flags", C.c_int32), ("reserved", C.c_int32 * 5)]
 
     @classmethod
-    def make(cls, tiling, depth, p, root_x, root_y, root_size, self_mode=False, rank=0, nranks=1):
+    def make(cls, tiling, depth, p, root_x, root_y, root_size, self_mode=False, rank=0, nranks=1, timing=False):
         return cls(_TILING[tiling], int(depth), int(p), int(bool(self_mode)), float(root_x), float(root_y),
-                   float(root_size), int(rank), int(nranks))
+                   float(root_size), int(rank), int(nranks), FLAG_TIMING if timing else 0)
 
 
 class FmmError(RuntimeError):
@@ -78,6 +79,8 @@ def lib():
             "fmm_stage_times": (C.c_int, [vp, P(C.c_float)]),
             "fmm_rank_range": (C.c_int, [vp, P(C.c_int64), P(C.c_int64)]),
             "fmm_launch_count": (C.c_int64, [vp]),
+            "fmm_pool_reserve": (C.c_int, [C.c_size_t]),
+            "fmm_tree_bytes": (C.c_size_t, [vp]),
             "fmm_free": (None, [vp]),
             "fmm_error_string": (C.c_char_p, [C.c_int]),
             "fmm_last_error_message": (C.c_char_p, []),
@@ -204,3 +207,14 @@ class Tree:
 
     def launch_count(self):
         return int(lib().fmm_launch_count(self.h))
+
+    def nbytes(self):
+        """device bytes of the tree's slab (fmm_tree_bytes)"""
+        return int(lib().fmm_tree_bytes(self.h))
+
+
+def pool_reserve(nbytes: int):
+    """grow the stream-ordered pool the trees allocate from (fmm_pool_reserve)"""
+    rc = lib().fmm_pool_reserve(int(nbytes))
+    if rc:
+        raise FmmError(rc, "fmm_pool_reserve")
