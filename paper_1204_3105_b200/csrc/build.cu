@@ -201,14 +201,16 @@ __global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const 
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t j = perm[i];
-  sxy[i] = xy[j];
+  const double2 v = xy[j];
+  sxy[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
   su[i] = u[j];
 }
 __global__ void k_gather_xy(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
                             double2* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  out[i] = xy[perm[i]];
+  const double2 v = xy[perm[i]];
+  out[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
 }
 
 // ------------------------------------------------------------------ centres (D12)

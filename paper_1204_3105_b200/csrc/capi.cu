@@ -92,6 +92,9 @@ int make_geo(const fmm_config* c, Geo* g) {
   if (c->p < 1 || c->p > FMM_MAX_P - 1) return FMM_EBADCFG;
   if (c->depth < 1 || c->depth > (c->tiling == FMM_SEPTREE ? 10 : 15)) return FMM_EBADCFG;
   if (!(c->root_size > 0.0) || !isfinite(c->root_x) || !isfinite(c->root_y)) return FMM_EBADCFG;
+  // the P2P kernel pads with points at |coordinate| 1e30 (p2p.cu): keep the domain far below
+  if (!(fabs(c->root_x) + 2.0 * c->root_size < 1e20 && fabs(c->root_y) + 2.0 * c->root_size < 1e20))
+    return FMM_EBADCFG;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return FMM_EBADCFG;
   for (int i = 0; i < 5; ++i)
     if (c->reserved[i]) return FMM_EBADCFG;

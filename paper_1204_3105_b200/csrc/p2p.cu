@@ -94,11 +94,50 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 }
 
 // ------------------------------------------------------------------ the pair kernel
-// Lane = (phase, row): row = lane % 8 (8 target rows of the block), phase = lane / 8 (4 source
-// columns per step).  Sources of s are staged 32 at a time in shared memory.
+// Lane = (row lane tl = lane % 4, phase ph = lane / 4).  A row step covers 8 target rows: the
+// lane owns rows tl and tl + 4.  Sources of s are staged 32 at a time in shared memory and a
+// lane visits columns 16 h + 8 j + ph (h, j in {0, 1}): 2 rows x 2 columns per (h) step.
+// Padding replaces every validity test in the pair loop: missing rows sit at (PAD, PAD) with
+// u = 0, missing columns at (-PAD, PAD) with u = 0 (coordinates are < 1e20 in magnitude,
+// make_geo), so their terms are exactly 0 and no pair of them is near.  The excluded pair
+// (i, i) of a diagonal block (D16) is the only z = 0 that is not an error.
 #ifndef P2P_MINB
 #define P2P_MINB 6  // resident blocks per SM the register allocation is sized for
 #endif
+constexpr double P2P_PAD = 1.0e30;
+
+struct PairOut {
+  double kd, lz, ag;  // log|z|^2 = kd ln 2 + lz, Arg z
+};
+
+// log|z|^2 and Arg z of z = y - x (D13: canonical +0 imaginary zero)
+__device__ __forceinline__ PairOut p2p_pair(double2 y, double2 x, const double2* s_log, const double2* s_atan,
+                                            bool self_ok, const int32_t* tperm, int trow, int scol,
+                                            DevStatus* st) {
+  const double dx = y.x - x.x, dy = y.y - x.y;
+  const double r2 = fma(dx, dx, dy * dy);
+  PairOut o;
+  if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
+    o.kd = 0.0;
+    if (r2 == 0.0) {
+      if (!self_ok) {  // coincident points: report the smallest caller index involved
+        unsigned long long bad = (unsigned long long)tperm[trow];
+        if (scol >= 0) bad = min(bad, (unsigned long long)tperm[scol]);
+        atomicMin(&st->coincident_bad, bad);
+      }
+      o.lz = 0.0;
+      o.ag = 0.0;
+    } else {
+      o.lz = 2.0 * log(hypot(dx, dy));
+      o.ag = atan2(__dadd_rn(dy, 0.0), dx);
+    }
+  } else {
+    p2p_log_split(r2, s_log, &o.kd, &o.lz);
+    o.ag = p2p_atan2(dy, dx, s_atan);
+  }
+  return o;
+}
+
 __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
@@ -110,10 +149,9 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
   __shared__ double2 s_xy[4][32];
   __shared__ double s_u[4][32];
   p2p_load_tables(tabs, s_log, s_atan);
-  const uint32_t a_log = (uint32_t)__cvta_generic_to_shared(s_log);
-  const uint32_t a_atan = (uint32_t)__cvta_generic_to_shared(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int tl = lane & 7, phase = lane >> 3;
+  const int tl = lane & 3, ph = lane >> 2;
+  const bool b1 = tl & 2, b0 = tl & 1;
   const double PI = 3.141592653589793;
   const int ntask = *ntask_p;
   while (true) {
@@ -129,89 +167,65 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const bool write_rows = t >= lo && t < hi;
     const bool write_react = sym && s >= lo && s < hi;
     for (int rc = tk.z; rc < tk.w; rc += 8) {
-      const int row = rc + tl;
-      const bool rvalid = row < tk.w;
-      const double2 y = rvalid ? txy[tb + row] : make_double2(1.0e5, 1.0e5);
-      const double urow = (sym && rvalid) ? su[tb + row] : 0.0;  // self mode: the row target is also a source
-      double acc_k = 0.0, acc_z = 0.0, acc_i = 0.0;
+      const int row0 = rc + tl, row1 = row0 + 4;
+      const bool v0 = row0 < tk.w, v1 = row1 < tk.w;
+      const double2 y0 = v0 ? txy[tb + row0] : make_double2(P2P_PAD, P2P_PAD);
+      const double2 y1 = v1 ? txy[tb + row1] : make_double2(P2P_PAD, P2P_PAD);
+      // self mode: the row targets are also sources (their strengths weight the reactions)
+      const double u0 = (sym && v0) ? su[tb + row0] : 0.0, u1 = (sym && v1) ? su[tb + row1] : 0.0;
+      double a0k = 0.0, a0z = 0.0, a0i = 0.0, a1k = 0.0, a1z = 0.0, a1i = 0.0;
       for (int c0 = 0; c0 < ns; c0 += 32) {
         if (c0 + lane < ns) {
           s_xy[w][lane] = sxy[sb + c0 + lane];
           s_u[w][lane] = su[sb + c0 + lane];
+        } else {
+          s_xy[w][lane] = make_double2(-P2P_PAD, P2P_PAD);
+          s_u[w][lane] = 0.0;
         }
         __syncwarp();
         const int cnt = min(32, ns - c0);
-        // reaction on this lane's column of the chunk, k_own = 4 * (4 * b0 + 2 * b2 + b1) + phase
-        // (tl = b2 b1 b0): see the reduce-scatter below
+        // reaction of this lane's column 16 b0 + 8 b1 + ph of the chunk (reduce-scatter below)
         double R_re = 0.0, R_im = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
-          double vr[4], vi[4];
+          double vr[2], vi[2];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int k = 4 * (4 * h + j) + phase;
-            const bool valid = k < cnt && rvalid;
+          for (int j = 0; j < 2; ++j) {
+            const int k = 16 * h + 8 * j + ph;
             const double2 x = s_xy[w][k];
-            const double uc = valid ? s_u[w][k] : 0.0;
-            double dx = y.x - x.x, dy = y.y - x.y;
-            // excluded pair (i, i) of a diagonal block (D16) and padding: z := 1 + 0i gives
-            // log|z|^2 = 0 and Arg z = 0 exactly
-            if (!valid || (diag && c0 + k == row)) {
-              dx = 1.0;
-              dy = 0.0;
-            }
-            const double r2 = fma(dx, dx, dy * dy);
-            double kd, lz, ag;
-            if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
-              kd = 0.0;
-              if (r2 == 0.0) {
-                unsigned long long bad = tperm[tb + row];
-                if (sym) bad = min(bad, (unsigned long long)tperm[sb + c0 + k]);
-                atomicMin(&st->coincident_bad, bad);
-                lz = 0.0;
-                ag = 0.0;
-              } else {
-                lz = 2.0 * log(hypot(dx, dy));
-                ag = atan2(__dadd_rn(dy, 0.0), dx);
-              }
-            } else {
-              p2p_log_split(r2, a_log, &kd, &lz);
-              ag = p2p_atan2(dy, dx, a_atan);
-            }
-            acc_k = fma(uc, kd, acc_k);
-            acc_z = fma(uc, lz, acc_z);
-            acc_i = fma(uc, ag, acc_i);
-            // reversed pair: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
-            vr[j] = urow * fma(kd, P2P_C[10], lz);
-            vi[j] = urow * (ag > 0.0 ? ag - PI : ag + PI);
+            const double uc = s_u[w][k];
+            const int col = c0 + k;
+            const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
+            const PairOut p0 = p2p_pair(y0, x, s_log, s_atan, diag && col == row0, tperm, tb + row0, scol, st);
+            const PairOut p1 = p2p_pair(y1, x, s_log, s_atan, diag && col == row1, tperm, tb + row1, scol, st);
+            a0k = fma(uc, p0.kd, a0k);
+            a0z = fma(uc, p0.lz, a0z);
+            a0i = fma(uc, p0.ag, a0i);
+            a1k = fma(uc, p1.kd, a1k);
+            a1z = fma(uc, p1.lz, a1z);
+            a1i = fma(uc, p1.ag, a1i);
+            // reversed pairs: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
+            vr[j] = fma(u0, fma(p0.kd, P2P_C[12], p0.lz), u1 * fma(p1.kd, P2P_C[12], p1.lz));
+            vi[j] = fma(u0, p0.ag > 0.0 ? p0.ag - PI : p0.ag + PI, u1 * (p1.ag > 0.0 ? p1.ag - PI : p1.ag + PI));
           }
           if (sym) {
-            // reduce-scatter over the 8 row lanes (tl) of this phase: halving xor 4, 2, then
-            // the xor-1 pair adds; lane (b2 b1 b0) ends with column j = 2 b2 + b1 of group h
-            const bool b2 = tl & 4, b1 = tl & 2, b0 = tl & 1;
-            double s0r = b2 ? vr[0] : vr[2], s0i = b2 ? vi[0] : vi[2];
-            double s1r = b2 ? vr[1] : vr[3], s1i = b2 ? vi[1] : vi[3];
-            double k0r = b2 ? vr[2] : vr[0], k0i = b2 ? vi[2] : vi[0];
-            double k1r = b2 ? vr[3] : vr[1], k1i = b2 ? vi[3] : vi[1];
-            k0r += __shfl_xor_sync(0xffffffffu, s0r, 4);
-            k0i += __shfl_xor_sync(0xffffffffu, s0i, 4);
-            k1r += __shfl_xor_sync(0xffffffffu, s1r, 4);
-            k1i += __shfl_xor_sync(0xffffffffu, s1i, 4);
-            double sr = b1 ? k0r : k1r, si = b1 ? k0i : k1i;
-            double mr = b1 ? k1r : k0r, mi = b1 ? k1i : k0i;
-            mr += __shfl_xor_sync(0xffffffffu, sr, 2);
-            mi += __shfl_xor_sync(0xffffffffu, si, 2);
-            mr += __shfl_xor_sync(0xffffffffu, mr, 1);
-            mi += __shfl_xor_sync(0xffffffffu, mi, 1);
+            // reduce-scatter over the 4 row lanes: xor 2 halves (lane keeps column j = b1),
+            // xor 1 completes; lane (b1, b0 = h) keeps column 16 h + 8 b1 + ph
+            double kr = b1 ? vr[1] : vr[0], ki = b1 ? vi[1] : vi[0];
+            const double sr = b1 ? vr[0] : vr[1], si = b1 ? vi[0] : vi[1];
+            kr += __shfl_xor_sync(0xffffffffu, sr, 2);
+            ki += __shfl_xor_sync(0xffffffffu, si, 2);
+            kr += __shfl_xor_sync(0xffffffffu, kr, 1);
+            ki += __shfl_xor_sync(0xffffffffu, ki, 1);
             if ((int)b0 == h) {
-              R_re = mr;
-              R_im = mi;
+              R_re = kr;
+              R_im = ki;
             }
           }
         }
         if (write_react) {
-          const int k = 4 * (4 * (tl & 1) + 2 * ((tl >> 2) & 1) + ((tl >> 1) & 1)) + phase;
+          const int k = 16 * (int)b0 + 8 * (int)b1 + ph;
           if (k < cnt) {
             double2* slot = part + ((int64_t)(sb + c0 + k) * nslot + qr);
             if (rc == tk.z) {
@@ -224,16 +238,19 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
         }
         __syncwarp();
       }
-      // reduce the 4 phases of each row (lanes tl, tl+8, tl+16, tl+24)
+      // reduce the 8 phases of each row (lanes tl + 4 ph)
 #pragma unroll
-      for (int o = 8; o < 32; o <<= 1) {
-        acc_k += __shfl_xor_sync(0xffffffffu, acc_k, o);
-        acc_z += __shfl_xor_sync(0xffffffffu, acc_z, o);
-        acc_i += __shfl_xor_sync(0xffffffffu, acc_i, o);
+      for (int o = 4; o < 32; o <<= 1) {
+        a0k += __shfl_xor_sync(0xffffffffu, a0k, o);
+        a0z += __shfl_xor_sync(0xffffffffu, a0z, o);
+        a0i += __shfl_xor_sync(0xffffffffu, a0i, o);
+        a1k += __shfl_xor_sync(0xffffffffu, a1k, o);
+        a1z += __shfl_xor_sync(0xffffffffu, a1z, o);
+        a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
       }
-      if (phase == 0 && rvalid && write_rows) {
-        const double re = fma(acc_k, P2P_C[10], acc_z) + acc_k * P2P_C[11];  // + ln 2 * sum u k
-        part[(int64_t)(tb + row) * nslot + q] = make_double2(re, acc_i);
+      if (ph == 0 && write_rows) {
+        if (v0) part[(int64_t)(tb + row0) * nslot + q] = make_double2(fma(a0k, P2P_C[10], a0z) + a0k * P2P_C[11], a0i);
+        if (v1) part[(int64_t)(tb + row1) * nslot + q] = make_double2(fma(a1k, P2P_C[10], a1z) + a1k * P2P_C[11], a1i);
       }
     }
   }
@@ -284,10 +301,9 @@ __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const
   p2p_load_tables(tabs, s_log, s_atan);
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double dx = d[i].x, dy = d[i].y;
-  double r2 = fma(dx, dx, dy * dy);
-  out[i] = make_double2(p2p_log(r2, (uint32_t)__cvta_generic_to_shared(s_log)),
-                        p2p_atan2(dy, dx, (uint32_t)__cvta_generic_to_shared(s_atan)));
+  const double dx = d[i].x, dy = __dadd_rn(d[i].y, 0.0);  // canonical +0 imaginary zero (D13)
+  const double r2 = fma(dx, dx, dy * dy);
+  out[i] = make_double2(p2p_log(r2, s_log), p2p_atan2(dy, dx, s_atan));
 }
 
 }  // namespace

@@ -33,26 +33,19 @@
 #define P2P_LOG_OFF_HI 0x3fe5f000
 #define P2P_LOG_OFF 0x3fe5f00000000000ull
 
-__constant__ double P2P_C[12] = {
+__constant__ double P2P_C[13] = {
     1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,  // log1p Taylor r^7 .. r^2
     1.0 / 9.0, -1.0 / 7.0, 1.0 / 5.0, -1.0 / 3.0,                   // atan Taylor q^9 .. q^3
-    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45                      // ln 2 = hi (42 bits) + lo
+    0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45,                     // ln 2 = hi (42 bits) + lo
+    0x1.62e42fefa39efp-1                                             // ln 2 (double)
 };
 
-// copy the tables to shared memory (whole block; ends with __syncthreads); the math
-// functions take the tables' 32-bit shared-space addresses (hoisted out of the pair loop)
+// copy the tables to shared memory (whole block; ends with __syncthreads)
 __device__ __forceinline__ void p2p_load_tables(const double* __restrict__ tabs, double2* s_log, double2* s_atan) {
   const double2* t2 = (const double2*)tabs;
   for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
   for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATAN / 2 + i];
   __syncthreads();
-}
-
-// 16-byte load from a shared-space (32-bit) address
-__device__ __forceinline__ double2 p2p_lds2(uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
 }
 
 __device__ __forceinline__ double p2p_rcp(double b) {
@@ -69,25 +62,16 @@ __device__ __forceinline__ float p2p_rcpf(float x) {
   return r;
 }
 
-// |x| as binary32 by truncation of the binary64 pattern (exponent rebias with a clamp at 0)
-__device__ __forceinline__ float p2p_d2f_trunc(double x) {
-  int h = __double2hiint(x) & 0x7fffffff;
-  int lo = __double2loint(x);
-  int e = max((h >> 20) - (1023 - 127), 0);  // binary32 biased exponent (0 -> ~0)
-  int m = ((h & 0xfffff) << 3) | ((unsigned)lo >> 29);
-  return __int_as_float(e > 0 ? ((e << 23) | m) : 0);
-}
-
 // log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
 // The 128 intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
-__device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
+__device__ __forceinline__ void p2p_log_split(double r2, const double2* logtab, double* kd, double* lz) {
   int hi = __double2hiint(r2), lo = __double2loint(r2);
   int tmp = hi - P2P_LOG_OFF_HI;
   int i = (tmp >> 13) & (P2P_LOG_N - 1);
   int k = tmp >> 20;  // arithmetic shift
   double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
-  double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
+  const double2 cl = logtab[i];  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
   // r^5..r^7 coefficients rounded to 20-bit mantissas (SASS immediates): their error
@@ -101,14 +85,16 @@ __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double
   *kd = (double)k;
 }
 
-__device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
+__device__ __forceinline__ double p2p_log(double r2, const double2* logtab) {
   double kd, lz;
   p2p_log_split(r2, logtab, &kd, &lz);
   return fma(kd, P2P_C[10], lz) + kd * P2P_C[11];
 }
 
-// Arg(dx + i dy) in (-pi, pi], a zero imaginary part read as +0 (D13); |z| >= 1e-30
-__device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
+// Arg(dx + i dy) in (-pi, pi] for |z| >= 1e-30.  dy must not be -0: callers pass a
+// canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
+// so y - x never yields -0 there).
+__device__ __forceinline__ double p2p_atan2(double dy, double dx, const double2* atab) {
   // FP32 estimate of t = min/max of |dx|, |dy| (|z| >= 1e-30 keeps the larger one a normal
   // binary32; a smaller one that flushes to 0 only means t ~ 0)
   float fx = fabsf(__double2float_rn(dx)), fy = fabsf(__double2float_rn(dy));
@@ -118,11 +104,10 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   double num = swap ? dx : dy, den = swap ? dy : dx;
   num = fabs(num);
   den = fabs(den);
-  // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0 (dy = -0 counts as +0)
-  int hx = __double2hiint(dx), hy = __double2hiint(dy);
-  bool dyneg = (hy < 0) && (((hy & 0x7fffffff) | __double2loint(dy)) != 0);
-  int oct = (int)swap | ((hx >> 31) & 2) | ((int)dyneg << 2);
-  double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (T[oct][k], t_k)
+  // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
+  const int hx = __double2hiint(dx), hy = __double2hiint(dy);
+  const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
+  const double2 Tt = atab[oct * (P2P_ATAN_K + 1) + k];  // (T[oct][k], t_k)
   double a = fma(-Tt.y, den, num);
   double b = fma(Tt.y, num, den);
   double q = a * p2p_rcp(b);
@@ -133,7 +118,7 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   P = fma(P, q2, P2P_C[9]);  // -1/3
   double at = fma(q * q2, P, q);
   // sign S = (-1)^(swap + dxneg + dyneg) applied by flipping the sign bit
-  int par = ((int)swap ^ (int)dyneg ^ (hx >> 31)) & 1;
-  at = __hiloint2double(__double2hiint(at) ^ (par << 31), __double2loint(at));
+  const int sgn = (hx ^ hy ^ (swap ? 0x80000000 : 0)) & 0x80000000;
+  at = __hiloint2double(__double2hiint(at) ^ sgn, __double2loint(at));
   return Tt.x + at;
 }
