@@ -105,34 +105,36 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 #define P2P_MINB 6  // resident blocks per SM the register allocation is sized for
 #endif
 constexpr double P2P_PAD = 1.0e30;
+constexpr int P2P_S = 160;  // sources of one near leaf kept in shared memory per warp
 
 struct PairOut {
-  double kd, lz, ag;  // log|z|^2 = kd ln 2 + lz, Arg z
+  double lg, ag;  // log|z|^2, Arg z
 };
 
 // log|z|^2 and Arg z of z = y - x (D13: canonical +0 imaginary zero)
-__device__ __forceinline__ PairOut p2p_pair(double2 y, double2 x, const double2* s_log, const double2* s_atan,
+__device__ __forceinline__ PairOut p2p_pair(double2 y, double2 x, uint32_t s_log, uint32_t s_atan,
                                             bool self_ok, const int32_t* tperm, int trow, int scol,
                                             DevStatus* st) {
   const double dx = y.x - x.x, dy = y.y - x.y;
   const double r2 = fma(dx, dx, dy * dy);
   PairOut o;
   if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
-    o.kd = 0.0;
     if (r2 == 0.0) {
       if (!self_ok) {  // coincident points: report the smallest caller index involved
         unsigned long long bad = (unsigned long long)tperm[trow];
         if (scol >= 0) bad = min(bad, (unsigned long long)tperm[scol]);
         atomicMin(&st->coincident_bad, bad);
       }
-      o.lz = 0.0;
+      o.lg = 0.0;
       o.ag = 0.0;
     } else {
-      o.lz = 2.0 * log(hypot(dx, dy));
+      o.lg = 2.0 * log(hypot(dx, dy));
       o.ag = atan2(__dadd_rn(dy, 0.0), dx);
     }
   } else {
-    p2p_log_split(r2, s_log, &o.kd, &o.lz);
+    double kd, lz;
+    p2p_log_split(r2, s_log, &kd, &lz);
+    o.lg = fma(kd, P2P_C[12], lz);  // kd ln 2 + lz (one rounding of the exact product sum)
     o.ag = p2p_atan2(dy, dx, s_atan);
   }
   return o;
@@ -146,9 +148,11 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     int64_t lo, int64_t hi, DevStatus* st) {
   __shared__ double2 s_log[P2P_LOG_N];
   __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
-  __shared__ double2 s_xy[4][32];
-  __shared__ double s_u[4][32];
+  __shared__ double2 s_xy[4][P2P_S];  // the sources of s (or a 32-chunk of them)
+  __shared__ double s_u[4][P2P_S];
+  __shared__ double2 s_re[4][P2P_S];  // reactions of the sources of s (self mode)
   p2p_load_tables(tabs, s_log, s_atan);
+  const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tl = lane & 3, ph = lane >> 2;
   const bool b1 = tl & 2, b0 = tl & 1;
@@ -166,6 +170,22 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const int tb = toff[t], sb = soff[s], ns = soff[s + 1] - sb;
     const bool write_rows = t >= lo && t < hi;
     const bool write_react = sym && s >= lo && s < hi;
+    // ns <= P2P_S: the sources (padded to a multiple of 32) stay in shared memory for the task
+    // and the reactions accumulate there; larger leaves are restaged per row step and chunk
+    const bool whole = ns <= P2P_S;
+    if (whole) {
+      for (int i = lane; i < ((ns + 31) & ~31); i += 32) {
+        if (i < ns) {
+          s_xy[w][i] = sxy[sb + i];
+          s_u[w][i] = su[sb + i];
+        } else {
+          s_xy[w][i] = make_double2(-P2P_PAD, P2P_PAD);
+          s_u[w][i] = 0.0;
+        }
+        s_re[w][i] = make_double2(0.0, 0.0);
+      }
+      __syncwarp();
+    }
     for (int rc = tk.z; rc < tk.w; rc += 8) {
       const int row0 = rc + tl, row1 = row0 + 4;
       const bool v0 = row0 < tk.w, v1 = row1 < tk.w;
@@ -173,40 +193,43 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
       const double2 y1 = v1 ? txy[tb + row1] : make_double2(P2P_PAD, P2P_PAD);
       // self mode: the row targets are also sources (their strengths weight the reactions)
       const double u0 = (sym && v0) ? su[tb + row0] : 0.0, u1 = (sym && v1) ? su[tb + row1] : 0.0;
-      double a0k = 0.0, a0z = 0.0, a0i = 0.0, a1k = 0.0, a1z = 0.0, a1i = 0.0;
+      double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
       for (int c0 = 0; c0 < ns; c0 += 32) {
-        if (c0 + lane < ns) {
-          s_xy[w][lane] = sxy[sb + c0 + lane];
-          s_u[w][lane] = su[sb + c0 + lane];
-        } else {
-          s_xy[w][lane] = make_double2(-P2P_PAD, P2P_PAD);
-          s_u[w][lane] = 0.0;
+        if (!whole) {
+          if (c0 + lane < ns) {
+            s_xy[w][lane] = sxy[sb + c0 + lane];
+            s_u[w][lane] = su[sb + c0 + lane];
+          } else {
+            s_xy[w][lane] = make_double2(-P2P_PAD, P2P_PAD);
+            s_u[w][lane] = 0.0;
+          }
+          __syncwarp();
         }
-        __syncwarp();
+        const int cb = whole ? c0 : 0;  // chunk base in shared memory
         const int cnt = min(32, ns - c0);
         // reaction of this lane's column 16 b0 + 8 b1 + ph of the chunk (reduce-scatter below)
         double R_re = 0.0, R_im = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
-          double vr[2], vi[2];
+          const bool two = cnt - 16 * h > 8;  // ... and an empty last quarter
+          double vr[2] = {0.0, 0.0}, vi[2] = {0.0, 0.0};
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
+            if (j == 1 && !two) break;
             const int k = 16 * h + 8 * j + ph;
-            const double2 x = s_xy[w][k];
-            const double uc = s_u[w][k];
+            const double2 x = s_xy[w][cb + k];
+            const double uc = s_u[w][cb + k];
             const int col = c0 + k;
             const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
-            const PairOut p0 = p2p_pair(y0, x, s_log, s_atan, diag && col == row0, tperm, tb + row0, scol, st);
-            const PairOut p1 = p2p_pair(y1, x, s_log, s_atan, diag && col == row1, tperm, tb + row1, scol, st);
-            a0k = fma(uc, p0.kd, a0k);
-            a0z = fma(uc, p0.lz, a0z);
+            const PairOut p0 = p2p_pair(y0, x, a_log, a_atan, diag && col == row0, tperm, tb + row0, scol, st);
+            const PairOut p1 = p2p_pair(y1, x, a_log, a_atan, diag && col == row1, tperm, tb + row1, scol, st);
+            a0r = fma(uc, p0.lg, a0r);
             a0i = fma(uc, p0.ag, a0i);
-            a1k = fma(uc, p1.kd, a1k);
-            a1z = fma(uc, p1.lz, a1z);
+            a1r = fma(uc, p1.lg, a1r);
             a1i = fma(uc, p1.ag, a1i);
             // reversed pairs: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
-            vr[j] = fma(u0, fma(p0.kd, P2P_C[12], p0.lz), u1 * fma(p1.kd, P2P_C[12], p1.lz));
+            vr[j] = fma(u0, p0.lg, u1 * p1.lg);
             vi[j] = fma(u0, p0.ag > 0.0 ? p0.ag - PI : p0.ag + PI, u1 * (p1.ag > 0.0 ? p1.ag - PI : p1.ag + PI));
           }
           if (sym) {
@@ -224,7 +247,11 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
             }
           }
         }
-        if (write_react) {
+        if (sym && whole) {  // this lane owns column k of the chunk for the whole task
+          const int k = cb + 16 * (int)b0 + 8 * (int)b1 + ph;
+          const double2 o = s_re[w][k];
+          s_re[w][k] = make_double2(o.x + R_re, o.y + R_im);
+        } else if (write_react) {
           const int k = 16 * (int)b0 + 8 * (int)b1 + ph;
           if (k < cnt) {
             double2* slot = part + ((int64_t)(sb + c0 + k) * nslot + qr);
@@ -236,23 +263,25 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
             }
           }
         }
-        __syncwarp();
+        if (!whole) __syncwarp();
       }
       // reduce the 8 phases of each row (lanes tl + 4 ph)
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) {
-        a0k += __shfl_xor_sync(0xffffffffu, a0k, o);
-        a0z += __shfl_xor_sync(0xffffffffu, a0z, o);
+        a0r += __shfl_xor_sync(0xffffffffu, a0r, o);
         a0i += __shfl_xor_sync(0xffffffffu, a0i, o);
-        a1k += __shfl_xor_sync(0xffffffffu, a1k, o);
-        a1z += __shfl_xor_sync(0xffffffffu, a1z, o);
+        a1r += __shfl_xor_sync(0xffffffffu, a1r, o);
         a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
       }
       if (ph == 0 && write_rows) {
-        if (v0) part[(int64_t)(tb + row0) * nslot + q] = make_double2(fma(a0k, P2P_C[10], a0z) + a0k * P2P_C[11], a0i);
-        if (v1) part[(int64_t)(tb + row1) * nslot + q] = make_double2(fma(a1k, P2P_C[10], a1z) + a1k * P2P_C[11], a1i);
+        if (v0) part[(int64_t)(tb + row0) * nslot + q] = make_double2(a0r, a0i);
+        if (v1) part[(int64_t)(tb + row1) * nslot + q] = make_double2(a1r, a1i);
       }
     }
+    __syncwarp();
+    if (whole && write_react)
+      for (int i = lane; i < ns; i += 32) part[(int64_t)(sb + i) * nslot + qr] = s_re[w][i];
+    __syncwarp();  // the next task restages s_xy / s_u / s_re
   }
 }
 
@@ -303,7 +332,7 @@ __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const
   if (i >= n) return;
   const double dx = d[i].x, dy = __dadd_rn(d[i].y, 0.0);  // canonical +0 imaginary zero (D13)
   const double r2 = fma(dx, dx, dy * dy);
-  out[i] = make_double2(p2p_log(r2, s_log), p2p_atan2(dy, dx, s_atan));
+  out[i] = make_double2(p2p_log(r2, p2p_smem_addr(s_log)), p2p_atan2(dy, dx, p2p_smem_addr(s_atan)));
 }
 
 }  // namespace

@@ -62,16 +62,31 @@ __device__ __forceinline__ float p2p_rcpf(float x) {
   return r;
 }
 
+// 16-byte load from a 32-bit shared-space address
+__device__ __forceinline__ double2 p2p_lds2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+// shared-space address of a table, laundered through an opaque move so that the compiler keeps
+// it in a register instead of re-deriving the shared window address at every use
+__device__ __forceinline__ uint32_t p2p_smem_addr(const void* p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+
 // log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
 // The 128 intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
-__device__ __forceinline__ void p2p_log_split(double r2, const double2* logtab, double* kd, double* lz) {
+__device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
   int hi = __double2hiint(r2), lo = __double2loint(r2);
   int tmp = hi - P2P_LOG_OFF_HI;
   int i = (tmp >> 13) & (P2P_LOG_N - 1);
   int k = tmp >> 20;  // arithmetic shift
   double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
-  const double2 cl = logtab[i];  // (1/c_i, log c_i)
+  const double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
   // r^5..r^7 coefficients rounded to 20-bit mantissas (SASS immediates): their error
@@ -85,7 +100,7 @@ __device__ __forceinline__ void p2p_log_split(double r2, const double2* logtab, 
   *kd = (double)k;
 }
 
-__device__ __forceinline__ double p2p_log(double r2, const double2* logtab) {
+__device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
   double kd, lz;
   p2p_log_split(r2, logtab, &kd, &lz);
   return fma(kd, P2P_C[10], lz) + kd * P2P_C[11];
@@ -94,7 +109,7 @@ __device__ __forceinline__ double p2p_log(double r2, const double2* logtab) {
 // Arg(dx + i dy) in (-pi, pi] for |z| >= 1e-30.  dy must not be -0: callers pass a
 // canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
 // so y - x never yields -0 there).
-__device__ __forceinline__ double p2p_atan2(double dy, double dx, const double2* atab) {
+__device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
   // FP32 estimate of t = min/max of |dx|, |dy| (|z| >= 1e-30 keeps the larger one a normal
   // binary32; a smaller one that flushes to 0 only means t ~ 0)
   float fx = fabsf(__double2float_rn(dx)), fy = fabsf(__double2float_rn(dy));
@@ -107,7 +122,7 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, const double2*
   // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
   const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
-  const double2 Tt = atab[oct * (P2P_ATAN_K + 1) + k];  // (T[oct][k], t_k)
+  const double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (T[oct][k], t_k)
   double a = fma(-Tt.y, den, num);
   double b = fma(Tt.y, num, den);
   double q = a * p2p_rcp(b);
