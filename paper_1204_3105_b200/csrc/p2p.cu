@@ -17,6 +17,7 @@
 namespace {
 
 constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) block
+constexpr int P2P_S = 160;          // sources of one near leaf kept in shared memory per warp
 constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
@@ -50,8 +51,15 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
       continue;
     }
     if (s < t) continue;  // the block belongs to the smaller leaf index
-    if (s == t) {
-      if (t_in) emit_rows(t, q, nt, ns, TF_DIAG);
+    if (s == t) {  // diagonal block: symmetric (each unordered pair once) when it fits a warp
+      if (t_in) {
+        if (ns <= P2P_S) {
+          if (out) out[c] = make_int4(t, q | (q << 8) | TF_SYM | TF_DIAG, 0, nt);
+          ++c;
+        } else {
+          emit_rows(t, q, nt, ns, TF_DIAG);
+        }
+      }
       continue;
     }
     const bool s_in = s >= lo && s < hi;
@@ -105,7 +113,6 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 #define P2P_MINB 6  // resident blocks per SM the register allocation is sized for
 #endif
 constexpr double P2P_PAD = 1.0e30;
-constexpr int P2P_S = 160;  // sources of one near leaf kept in shared memory per warp
 
 struct PairOut {
   double lg, ag;  // log|z|^2, Arg z
@@ -166,6 +173,12 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const int4 tk = tasks[task];
     const int t = tk.x, q = tk.y & 0xff, qr = (tk.y >> 8) & 0xff;
     const bool sym = tk.y & TF_SYM, diag = tk.y & TF_DIAG;
+    // symmetric diagonal block: a row step of rows [rc, rc + 8) and a 16-column half at a
+    // skips the half when a + 15 < rc (those pairs arrive as reactions of earlier row steps),
+    // evaluates it one-sided when it straddles the rows (a <= rc + 7; the pair (i, i) is the
+    // excluded z = 0) and symmetrically when it lies above them; each ordered pair i != j
+    // is then counted once (tests/test_p2p_schedule.py enumerates the rule)
+    const bool sd = sym && diag;
     const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
     const int tb = toff[t], sb = soff[s], ns = soff[s + 1] - sb;
     const bool write_rows = t >= lo && t < hi;
@@ -194,7 +207,7 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
       // self mode: the row targets are also sources (their strengths weight the reactions)
       const double u0 = (sym && v0) ? su[tb + row0] : 0.0, u1 = (sym && v1) ? su[tb + row1] : 0.0;
       double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
-      for (int c0 = 0; c0 < ns; c0 += 32) {
+      for (int c0 = sd ? (rc & ~31) : 0; c0 < ns; c0 += 32) {
         if (!whole) {
           if (c0 + lane < ns) {
             s_xy[w][lane] = sxy[sb + c0 + lane];
@@ -212,6 +225,9 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
+          const int a = c0 + 16 * h;
+          if (sd && a + 15 < rc) continue;
+          const bool react = sym && !(sd && a <= rc + 7);
           const bool two = cnt - 16 * h > 8;  // ... and an empty last quarter
           double vr[2] = {0.0, 0.0}, vi[2] = {0.0, 0.0};
 #pragma unroll
@@ -232,7 +248,7 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
             vr[j] = fma(u0, p0.lg, u1 * p1.lg);
             vi[j] = fma(u0, p0.ag > 0.0 ? p0.ag - PI : p0.ag + PI, u1 * (p1.ag > 0.0 ? p1.ag - PI : p1.ag + PI));
           }
-          if (sym) {
+          if (react) {
             // reduce-scatter over the 4 row lanes: xor 2 halves (lane keeps column j = b1),
             // xor 1 completes; lane (b1, b0 = h) keeps column 16 h + 8 b1 + ph
             double kr = b1 ? vr[1] : vr[0], ki = b1 ? vi[1] : vi[0];
@@ -273,7 +289,14 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
         a1r += __shfl_xor_sync(0xffffffffu, a1r, o);
         a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
       }
-      if (ph == 0 && write_rows) {
+      if (sd) {  // rows and reactions of a diagonal block share the slots: add the rows into s_re
+        __syncwarp();
+        if (ph == 0) {
+          if (v0) s_re[w][row0] = make_double2(s_re[w][row0].x + a0r, s_re[w][row0].y + a0i);
+          if (v1) s_re[w][row1] = make_double2(s_re[w][row1].x + a1r, s_re[w][row1].y + a1i);
+        }
+        __syncwarp();
+      } else if (ph == 0 && write_rows) {
         if (v0) part[(int64_t)(tb + row0) * nslot + q] = make_double2(a0r, a0i);
         if (v1) part[(int64_t)(tb + row1) * nslot + q] = make_double2(a1r, a1i);
       }
