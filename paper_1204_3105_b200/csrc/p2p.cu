@@ -118,31 +118,34 @@ struct PairOut {
   double lg, ag;  // log|z|^2, Arg z
 };
 
-// log|z|^2 and Arg z of z = y - x (D13: canonical +0 imaginary zero)
-__device__ __forceinline__ PairOut p2p_pair(double2 y, double2 x, uint32_t s_log, uint32_t s_atan,
-                                            bool self_ok, const int32_t* tperm, int trow, int scol,
-                                            DevStatus* st) {
-  const double dx = y.x - x.x, dy = y.y - x.y;
-  const double r2 = fma(dx, dx, dy * dy);
+// log|z|^2 and Arg z of z = dx + i dy for |z| >= 1e-30 (branch-free, so that the compiler
+// overlaps the pairs of a column).  Smaller |z| give finite table indices (s_atan is padded)
+// and garbage values, which p2p_slow replaces.
+__device__ __forceinline__ PairOut p2p_fast(double dx, double dy, double r2, uint32_t s_log, uint32_t s_atan) {
   PairOut o;
-  if (__double2hiint(r2) < P2P_SLOW_HI) {  // |z| < 1e-30 (incl. coincident): exact slow path
-    if (r2 == 0.0) {
-      if (!self_ok) {  // coincident points: report the smallest caller index involved
-        unsigned long long bad = (unsigned long long)tperm[trow];
-        if (scol >= 0) bad = min(bad, (unsigned long long)tperm[scol]);
-        atomicMin(&st->coincident_bad, bad);
-      }
-      o.lg = 0.0;
-      o.ag = 0.0;
-    } else {
-      o.lg = 2.0 * log(hypot(dx, dy));
-      o.ag = atan2(__dadd_rn(dy, 0.0), dx);
+  double kd, lz;
+  p2p_log_split(r2, s_log, &kd, &lz);
+  o.lg = fma(kd, P2P_C[12], lz);  // kd ln 2 + lz (one rounding of the exact product sum)
+  o.ag = p2p_atan2(dy, dx, s_atan);
+  return o;
+}
+
+// |z| < 1e-30: exact libdevice path; z = 0 is the excluded pair (i, i) of a diagonal block
+// (D16) or coincident points (an error: the smallest caller index involved is reported)
+__device__ __noinline__ PairOut p2p_slow(double dx, double dy, double r2, bool self_ok, const int32_t* tperm,
+                                         int trow, int scol, DevStatus* st) {
+  PairOut o;
+  if (r2 == 0.0) {
+    if (!self_ok) {
+      unsigned long long bad = (unsigned long long)tperm[trow];
+      if (scol >= 0) bad = min(bad, (unsigned long long)tperm[scol]);
+      atomicMin(&st->coincident_bad, bad);
     }
+    o.lg = 0.0;
+    o.ag = 0.0;
   } else {
-    double kd, lz;
-    p2p_log_split(r2, s_log, &kd, &lz);
-    o.lg = fma(kd, P2P_C[12], lz);  // kd ln 2 + lz (one rounding of the exact product sum)
-    o.ag = p2p_atan2(dy, dx, s_atan);
+    o.lg = 2.0 * log(hypot(dx, dy));
+    o.ag = atan2(__dadd_rn(dy, 0.0), dx);  // D13
   }
   return o;
 }
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     const int32_t* __restrict__ tperm, const double* __restrict__ tabs, double2* __restrict__ part, int nslot,
     int64_t lo, int64_t hi, DevStatus* st) {
   __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1) + 32];  // + pad: garbage indices of |z| < 1e-30
   __shared__ double2 s_xy[4][P2P_S];  // the sources of s (or a 32-chunk of them)
   __shared__ double s_u[4][P2P_S];
   __shared__ double2 s_re[4][P2P_S];  // reactions of the sources of s (self mode)
@@ -238,8 +241,15 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
             const double uc = s_u[w][cb + k];
             const int col = c0 + k;
             const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
-            const PairOut p0 = p2p_pair(y0, x, a_log, a_atan, diag && col == row0, tperm, tb + row0, scol, st);
-            const PairOut p1 = p2p_pair(y1, x, a_log, a_atan, diag && col == row1, tperm, tb + row1, scol, st);
+            const double dx0 = y0.x - x.x, dy0 = y0.y - x.y, dx1 = y1.x - x.x, dy1 = y1.y - x.y;
+            const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
+            PairOut p0 = p2p_fast(dx0, dy0, r20, a_log, a_atan);
+            PairOut p1 = p2p_fast(dx1, dy1, r21, a_log, a_atan);
+            const bool sl0 = __double2hiint(r20) < P2P_SLOW_HI, sl1 = __double2hiint(r21) < P2P_SLOW_HI;
+            if (__builtin_expect(sl0 || sl1, 0)) {
+              if (sl0) p0 = p2p_slow(dx0, dy0, r20, diag && col == row0, tperm, tb + row0, scol, st);
+              if (sl1) p1 = p2p_slow(dx1, dy1, r21, diag && col == row1, tperm, tb + row1, scol, st);
+            }
             a0r = fma(uc, p0.lg, a0r);
             a0i = fma(uc, p0.ag, a0i);
             a1r = fma(uc, p1.lg, a1r);
