@@ -48,9 +48,21 @@ WORKLOADS = {
 # FP64 peak derived from the unit counts and clocks of the guides:
 # 148 SMs x 64 FP64 FMA/clk/SM x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-# FP64 flops executed by k_p2p_pairs per near-field interaction, from ncu
-# (sm__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on; profiles/r01/p2p_fp64.json)
-F_INT = {"C4q": 36.67, "C4s": 34.30, "C4t": 35.66, "C3": 71.40, "C5": 51.33}
+# SURVEY §8(d) algorithmic work per unit:
+#  * P2P: F_pair FP64 flops per near-field interaction (ordered target-source pair), measured by
+#    ncu on the one-pair-per-thread microbenchmark tools/fpair_micro.py: 46 flops of math
+#    (|z|^2, log|z|^2, Arg z) + 2 DADD (y - x) + 2 DFMA (strength products) = 52
+#    (profiles/r01/fp64_counts.json).  The symmetric self-mode kernel evaluates each unordered
+#    pair once, so it executes fewer flops than this per interaction (reported beside it).
+#  * M2L: the dense-operator count 8 (p+1)^2 flops per M2L op.
+F_PAIR = 52.0
+# FP64 flops k_p2p_pairs executes per interaction (ncu, sm__sass_thread_inst_executed_op_
+# {dfma,dadd,dmul}_pred_on; profiles/r01/fp64_counts.json), for the executed-rate line
+F_EXEC = {"C4q": 31.47, "C4s": 29.48, "C4t": 31.21}
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu --set full,
+# profiles/r01/ncu_p2p_<cfg>_v10.txt); C4 = mean over its three launches.  The writes are the
+# per-(target, near slot) partial sums (m x nslot x 16 B) that k_p2p_finish adds.
+P2P_DRAM_BYTES_PER_LAUNCH = {"C4q": 2.887e9, "C4s": 2.809e9, "C4t": 4.074e9, "C4": 3.257e9}
 
 
 def log(*a):
@@ -254,23 +266,31 @@ def run_gpu(args):
         return None
 
     # ---- roofline of the dominant kernel k_p2p_pairs (the near-field pair kernel), timed with
-    # CUDA events on its stream around each launch inside the timed region.  Its algorithmic
-    # work is expressed per near-field interaction (target, source) of the near lists:
-    # F_INT[tiling] = FP64 flops (2 DFMA + DADD + DMUL) the kernel executes per interaction,
-    # measured once by ncu on the same config (profiles/r01/p2p_fp64.json); the symmetric
-    # self-mode evaluation makes this less than the one-sided per-pair count.
+    # CUDA events on its stream around each launch inside the timed region: algorithmic flops =
+    # near-field interactions x F_PAIR; the executed FP64 rate (ncu counts per
+    # interaction x interactions / the same time) is reported beside it
     pairs = {nm: int(counters[nm][1]) for nm in names}
     pair_ms_avg = sum(pair_ms.values()) / args.steps
-    flops = sum(pairs[nm] * F_INT.get(nm, 0.0) for nm in names)
+    flops = sum(pairs[nm] for nm in names) * F_PAIR
     ach = flops / (pair_ms_avg / 1e3) / 1e12 if pair_ms_avg > 0 else 0.0
+    exec_fl = sum(pairs[nm] * F_EXEC[nm] for nm in names) if all(nm in F_EXEC for nm in names) else None
     roof = {"kernel": "k_p2p_pairs (P2P near field; L2P + final sum in k_p2p_finish)", "bound": "alu",
             "achieved": round(ach, 3), "peak": round(FP64_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
-            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": P2P_DRAM_BYTES_PER_LAUNCH.get(args.workload),
             "peak_source": "FP64 FMA: 148 SM x 64 /clk x 2 x 1.965 GHz (DESIGN.md §7); DFMA microbenchmark "
                            "34.2 TF/s (profiles/r01/fp64_peak.log)",
+            "f_pair_flops": F_PAIR,
             "interactions_per_s": sum(pairs.values()) / (pair_ms_avg / 1e3) if pair_ms_avg > 0 else 0.0,
-            "f_int_flops": {nm: F_INT.get(nm) for nm in names},
+            "executed_tflops": None if exec_fl is None or pair_ms_avg <= 0 else round(exec_fl / (pair_ms_avg / 1e3) / 1e12, 3),
             "kernel_ms_per_step": round(pair_ms_avg, 3)}
+    # M2L (+ L2L) on the FP64 tensor cores: the downward stage time against 8 (p+1)^2 per op
+    m2l_fl = sum(int(counters[nm][0]) * 8 * (inputs[nm][0].p + 1) ** 2 for nm in names)
+    down_avg = sum(down_ms.values()) / args.steps
+    m2l_ach = m2l_fl / (down_avg / 1e3) / 1e12 if down_avg > 0 else 0.0
+    roof_m2l = {"kernel": "k_down_mma (M2L on DMMA m8n8k4 + L2L), all levels", "bound": "alu",
+                "achieved": round(m2l_ach, 3), "peak": round(FP64_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
+                "frac": round(m2l_ach / FP64_PEAK_TFLOPS, 4), "flops_per_op": "8 (p+1)^2",
+                "stage_ms_per_step": round(down_avg, 3)}
 
     per_tiling = {nm: {"build_ms": build_ms[nm] / args.steps, "upward_ms": up_ms[nm] / args.steps,
                        "downward_ms": down_ms[nm] / args.steps, "p2p_pairs_kernel_ms": pair_ms[nm] / args.steps,
@@ -286,6 +306,7 @@ def run_gpu(args):
                    "tilings": names, "step": "fmm_build_tree + fmm_evaluate per tiling",
                    "l2": "inputs larger than L2 (>= 400 MB per tiling)", "per_tiling": per_tiling},
         "roofline": roof,
+        "roofline_m2l": roof_m2l,
         "e2e": {"value": total_targets / (e2e_ms / 1e3), "unit": "target evals/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
