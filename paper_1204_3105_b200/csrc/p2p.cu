@@ -109,9 +109,18 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 // u = 0, missing columns at (-PAD, PAD) with u = 0 (coordinates are < 1e20 in magnitude,
 // make_geo), so their terms are exactly 0 and no pair of them is near.  The excluded pair
 // (i, i) of a diagonal block (D16) is the only z = 0 that is not an error.
-#ifndef P2P_MINB
-#define P2P_MINB 6  // resident blocks per SM the register allocation is sized for
+#ifndef P2P_WARPS
+#define P2P_WARPS 8  // warps per block (the tables are shared by the block)
 #endif
+#ifndef P2P_MINB
+#define P2P_MINB 3  // resident blocks per SM the register allocation is sized for
+#endif
+constexpr int P2P_RS = 32;  // row stride (double2) of the reaction scratch; column c of row lane r sits at c ^ 2r
+                            // (conflict-free STS.128 / LDS.128)
+// dynamic shared memory of one block: tables, then per warp sources, strengths, reactions, scratch
+constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1) + 32);
+constexpr size_t P2P_WARP_BYTES = sizeof(double2) * (2 * P2P_S + 4 * P2P_RS) + sizeof(double) * P2P_S;
+constexpr size_t P2P_SMEM = P2P_TAB_BYTES + P2P_WARPS * P2P_WARP_BYTES;
 constexpr double P2P_PAD = 1.0e30;
 
 struct PairOut {
@@ -150,22 +159,23 @@ __device__ __noinline__ PairOut p2p_slow(double dx, double dy, double r2, bool s
   return o;
 }
 
-__global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
+__global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
     const double2* __restrict__ sxy, const double* __restrict__ su, const int32_t* __restrict__ near,
     const int32_t* __restrict__ tperm, const double* __restrict__ tabs, double2* __restrict__ part, int nslot,
     int64_t lo, int64_t hi, DevStatus* st) {
-  __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1) + 32];  // + pad: garbage indices of |z| < 1e-30
-  __shared__ double2 s_xy[4][P2P_S];  // the sources of s (or a 32-chunk of them)
-  __shared__ double s_u[4][P2P_S];
-  __shared__ double2 s_re[4][P2P_S];  // reactions of the sources of s (self mode)
+  extern __shared__ double2 smem[];
+  double2* s_log = smem;
+  double2* s_atan = s_log + P2P_LOG_N;  // + 32 pad: garbage indices of |z| < 1e-30
   p2p_load_tables(tabs, s_log, s_atan);
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2* const s_xy = (double2*)((char*)smem + P2P_TAB_BYTES + w * P2P_WARP_BYTES);  // sources of s
+  double2* const s_re = s_xy + P2P_S;    // reactions of the sources of s (self mode)
+  double2* const s_rs = s_re + P2P_S;    // [4 row lanes][P2P_RS] reaction partials of a chunk
+  double* const s_u = (double*)(s_rs + 4 * P2P_RS);
   const int tl = lane & 3, ph = lane >> 2;
-  const bool b1 = tl & 2, b0 = tl & 1;
   const double PI = 3.141592653589793;
   const int ntask = *ntask_p;
   while (true) {
@@ -192,13 +202,13 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     if (whole) {
       for (int i = lane; i < ((ns + 31) & ~31); i += 32) {
         if (i < ns) {
-          s_xy[w][i] = sxy[sb + i];
-          s_u[w][i] = su[sb + i];
+          s_xy[i] = sxy[sb + i];
+          s_u[i] = su[sb + i];
         } else {
-          s_xy[w][i] = make_double2(-P2P_PAD, P2P_PAD);
-          s_u[w][i] = 0.0;
+          s_xy[i] = make_double2(-P2P_PAD, P2P_PAD);
+          s_u[i] = 0.0;
         }
-        s_re[w][i] = make_double2(0.0, 0.0);
+        s_re[i] = make_double2(0.0, 0.0);
       }
       __syncwarp();
     }
@@ -213,18 +223,17 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
       for (int c0 = sd ? (rc & ~31) : 0; c0 < ns; c0 += 32) {
         if (!whole) {
           if (c0 + lane < ns) {
-            s_xy[w][lane] = sxy[sb + c0 + lane];
-            s_u[w][lane] = su[sb + c0 + lane];
+            s_xy[lane] = sxy[sb + c0 + lane];
+            s_u[lane] = su[sb + c0 + lane];
           } else {
-            s_xy[w][lane] = make_double2(-P2P_PAD, P2P_PAD);
-            s_u[w][lane] = 0.0;
+            s_xy[lane] = make_double2(-P2P_PAD, P2P_PAD);
+            s_u[lane] = 0.0;
           }
           __syncwarp();
         }
         const int cb = whole ? c0 : 0;  // chunk base in shared memory
         const int cnt = min(32, ns - c0);
-        // reaction of this lane's column 16 b0 + 8 b1 + ph of the chunk (reduce-scatter below)
-        double R_re = 0.0, R_im = 0.0;
+        unsigned hw = 0;  // halves of the chunk whose reaction partials are in s_rs
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
@@ -237,8 +246,8 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
           for (int j = 0; j < 2; ++j) {
             if (j == 1 && !two) break;
             const int k = 16 * h + 8 * j + ph;
-            const double2 x = s_xy[w][cb + k];
-            const double uc = s_u[w][cb + k];
+            const double2 x = s_xy[cb + k];
+            const double uc = s_u[cb + k];
             const int col = c0 + k;
             const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
             const double dx0 = y0.x - x.x, dy0 = y0.y - x.y, dx1 = y1.x - x.x, dy1 = y1.y - x.y;
@@ -258,38 +267,37 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
             vr[j] = fma(u0, p0.lg, u1 * p1.lg);
             vi[j] = fma(u0, p0.ag > 0.0 ? p0.ag - PI : p0.ag + PI, u1 * (p1.ag > 0.0 ? p1.ag - PI : p1.ag + PI));
           }
-          if (react) {
-            // reduce-scatter over the 4 row lanes: xor 2 halves (lane keeps column j = b1),
-            // xor 1 completes; lane (b1, b0 = h) keeps column 16 h + 8 b1 + ph
-            double kr = b1 ? vr[1] : vr[0], ki = b1 ? vi[1] : vi[0];
-            const double sr = b1 ? vr[0] : vr[1], si = b1 ? vi[0] : vi[1];
-            kr += __shfl_xor_sync(0xffffffffu, sr, 2);
-            ki += __shfl_xor_sync(0xffffffffu, si, 2);
-            kr += __shfl_xor_sync(0xffffffffu, kr, 1);
-            ki += __shfl_xor_sync(0xffffffffu, ki, 1);
-            if ((int)b0 == h) {
-              R_re = kr;
-              R_im = ki;
-            }
+          if (react) {  // the 4 row lanes' partials of the 2 columns, summed below
+            s_rs[tl * P2P_RS + ((16 * h + ph) ^ (2 * tl))] = make_double2(vr[0], vi[0]);
+            s_rs[tl * P2P_RS + ((16 * h + 8 + ph) ^ (2 * tl))] = make_double2(vr[1], vi[1]);
+            hw |= 1u << h;
           }
         }
-        if (sym && whole) {  // this lane owns column k of the chunk for the whole task
-          const int k = cb + 16 * (int)b0 + 8 * (int)b1 + ph;
-          const double2 o = s_re[w][k];
-          s_re[w][k] = make_double2(o.x + R_re, o.y + R_im);
-        } else if (write_react) {
-          const int k = 16 * (int)b0 + 8 * (int)b1 + ph;
-          if (k < cnt) {
-            double2* slot = part + ((int64_t)(sb + c0 + k) * nslot + qr);
+        if (hw) {  // lane c owns column c of the chunk: add its 4 row-lane partials (fixed order)
+          __syncwarp();
+          double Rr = 0.0, Ri = 0.0;
+          if ((hw >> (lane >> 4)) & 1) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const double2 v = s_rs[r * P2P_RS + (lane ^ (2 * r))];
+              Rr += v.x;
+              Ri += v.y;
+            }
+          }
+          if (whole) {
+            const double2 o = s_re[cb + lane];
+            s_re[cb + lane] = make_double2(o.x + Rr, o.y + Ri);
+          } else if (write_react && lane < cnt) {
+            double2* slot = part + ((int64_t)(sb + c0 + lane) * nslot + qr);
             if (rc == tk.z) {
-              *slot = make_double2(R_re, R_im);
+              *slot = make_double2(Rr, Ri);
             } else {
               const double2 o = *slot;
-              *slot = make_double2(o.x + R_re, o.y + R_im);
+              *slot = make_double2(o.x + Rr, o.y + Ri);
             }
           }
         }
-        if (!whole) __syncwarp();
+        __syncwarp();
       }
       // reduce the 8 phases of each row (lanes tl + 4 ph)
 #pragma unroll
@@ -302,8 +310,8 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
       if (sd) {  // rows and reactions of a diagonal block share the slots: add the rows into s_re
         __syncwarp();
         if (ph == 0) {
-          if (v0) s_re[w][row0] = make_double2(s_re[w][row0].x + a0r, s_re[w][row0].y + a0i);
-          if (v1) s_re[w][row1] = make_double2(s_re[w][row1].x + a1r, s_re[w][row1].y + a1i);
+          if (v0) s_re[row0] = make_double2(s_re[row0].x + a0r, s_re[row0].y + a0i);
+          if (v1) s_re[row1] = make_double2(s_re[row1].x + a1r, s_re[row1].y + a1i);
         }
         __syncwarp();
       } else if (ph == 0 && write_rows) {
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(128, P2P_MINB) k_p2p_pairs(
     }
     __syncwarp();
     if (whole && write_react)
-      for (int i = lane; i < ns; i += 32) part[(int64_t)(sb + i) * nslot + qr] = s_re[w][i];
+      for (int i = lane; i < ns; i += 32) part[(int64_t)(sb + i) * nslot + qr] = s_re[i];
     __syncwarp();  // the next task restages s_xy / s_u / s_re
   }
 }
@@ -393,7 +401,8 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   const Geo& G = t->g;
   cudaStream_t s = t->stream;
   FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
-  k_p2p_pairs<<<148 * 6, 128, 0, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_p2p_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_SMEM));
+  k_p2p_pairs<<<148 * P2P_MINB, 32 * P2P_WARPS, P2P_SMEM, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
                                        t->near, t->tperm, t->p2p_tab, t->part, G.nslot, t->leaf_lo, t->leaf_hi, t->status);
   if (t->timing) cudaEventRecord(t->ev[7], s);
   const int64_t nl = t->leaf_hi - t->leaf_lo;
