@@ -237,12 +237,11 @@ __device__ inline void sort_small(int64_t* v, int n) {
   }
 }
 
-// One thread per parent P at level l-1.  Candidates = Children(P U Neighbors(P, l-1))
-// with sources, ascending; for every child t with targets, e4mask bit i is set iff
-// cand[i] is not in {t} U Neighbors(t, l)  (NeighborsE4, reading D1).
-__global__ void k_lists_level(DGeo g, int l, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
-                              int32_t* __restrict__ cand, int32_t* __restrict__ ncand,
-                              unsigned long long* __restrict__ e4mask, int64_t leaf_lo, int64_t leaf_hi) {
+// Candidates, one thread per parent P at level l-1: Children(P U Neighbors(P, l-1)) with
+// sources, ascending (none when no child of P has targets of this rank).
+__global__ void k_cand_level(DGeo g, int l, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                             int32_t* __restrict__ cand, int32_t* __restrict__ ncand, int64_t leaf_lo,
+                             int64_t leaf_hi) {
   int64_t P = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t nparents = ipow_d(g.B, l - 1);
   if (P >= nparents) return;
@@ -252,13 +251,11 @@ __global__ void k_lists_level(DGeo g, int l, const int32_t* __restrict__ soff, c
   int64_t lo = P * span_p, hi = lo + span_p;
   bool has_t = (hi > leaf_lo && lo < leaf_hi) &&
                (toff[min(hi, leaf_hi)] - toff[max(lo, leaf_lo)] > 0);
-  int32_t* my = cand + P * FMM_CAND_MAX;
-  unsigned long long* masks = e4mask;  // level-local
   if (!has_t) {
     ncand[P] = 0;
-    for (int ch = 0; ch < B; ++ch) masks[P * B + ch] = 0ull;
     return;
   }
+  int32_t* my = cand + P * FMM_CAND_MAX;
   int64_t pn[16];
   int npn = geo_neighbors(g, l - 1, P, pn);
   int64_t c[FMM_CAND_MAX];
@@ -273,22 +270,33 @@ __global__ void k_lists_level(DGeo g, int l, const int32_t* __restrict__ soff, c
   sort_small(c, nc);
   for (int i = 0; i < nc; ++i) my[i] = (int32_t)c[i];
   ncand[P] = nc;
-  for (int ch = 0; ch < B; ++ch) {
-    int64_t t = P * B + ch;
-    int64_t tl = t * span_l, th = tl + span_l;
-    bool t_has = (th > leaf_lo && tl < leaf_hi) && (toff[min(th, leaf_hi)] - toff[max(tl, leaf_lo)] > 0);
-    unsigned long long mask = 0ull;
-    if (t_has) {
-      int64_t nb[16];
-      int nn = geo_neighbors(g, l, t, nb);
-      for (int i = 0; i < nc; ++i) {
-        bool near = (c[i] == t);
-        for (int k = 0; k < nn; ++k) near |= (c[i] == nb[k]);
-        if (!near) mask |= 1ull << i;
-      }
+}
+
+// E4 masks, one thread per cell t at level l: bit i set iff cand[parent][i] is not in
+// {t} U Neighbors(t, l)  (NeighborsE4, reading D1); 0 when t has no targets.
+__global__ void k_e4mask_level(DGeo g, int l, const int32_t* __restrict__ toff, const int32_t* __restrict__ cand,
+                               const int32_t* __restrict__ ncand, unsigned long long* __restrict__ e4mask,
+                               int64_t leaf_lo, int64_t leaf_hi) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ipow_d(g.B, l)) return;
+  int64_t span_l = ipow_d(g.B, g.L - l);
+  int64_t tl = t * span_l, th = tl + span_l;
+  bool t_has = (th > leaf_lo && tl < leaf_hi) && (toff[min(th, leaf_hi)] - toff[max(tl, leaf_lo)] > 0);
+  unsigned long long mask = 0ull;
+  if (t_has) {
+    const int64_t P = t / g.B;
+    const int nc = ncand[P];
+    const int32_t* c = cand + P * FMM_CAND_MAX;
+    int64_t nb[16];
+    int nn = geo_neighbors(g, l, t, nb);
+    for (int i = 0; i < nc; ++i) {
+      const int64_t ci = c[i];
+      bool near = (ci == t);
+      for (int k = 0; k < nn; ++k) near |= (ci == nb[k]);
+      if (!near) mask |= 1ull << i;
     }
-    masks[t] = mask;
   }
+  e4mask[t] = mask;
 }
 
 // near(t) = ({t} U Neighbors(t, L)) with sources, ascending
@@ -498,10 +506,12 @@ int fmm_stage_tables_lists(fmm_tree_s* t) {
   if (e) return e;
   for (int l = 1; l <= G.L; ++l) {
     int64_t np = G.ncells[l - 1];
-    k_lists_level<<<blocks_for(np, 128), 128, 0, s>>>(g, l, t->soff, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
-                                                      t->ncand + G.lvl_off[l - 1], t->e4mask + G.lvl_off[l],
-                                                      t->leaf_lo, t->leaf_hi);
-    t->launches++;
+    k_cand_level<<<blocks_for(np, 128), 128, 0, s>>>(g, l, t->soff, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
+                                                     t->ncand + G.lvl_off[l - 1], t->leaf_lo, t->leaf_hi);
+    k_e4mask_level<<<blocks_for(G.ncells[l], 128), 128, 0, s>>>(g, l, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
+                                                                t->ncand + G.lvl_off[l - 1], t->e4mask + G.lvl_off[l],
+                                                                t->leaf_lo, t->leaf_hi);
+    t->launches += 2;
   }
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;

@@ -299,25 +299,29 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
         }
         __syncwarp();
       }
-      // reduce the 8 phases of each row (lanes tl + 4 ph)
+      // reduce the 8 phases of each row (lanes tl + 4 ph) through the scratch: lane (tl, ph)
+      // stores its two rows' sums; lane L < 16 adds component L & 1 of row L >> 1 over ph
+      // (fixed order)
+      s_rs[ph * 8 + tl] = make_double2(a0r, a0i);
+      s_rs[ph * 8 + 4 + tl] = make_double2(a1r, a1i);
+      __syncwarp();
+      if (lane < 16) {
+        const double* sd_ = (const double*)s_rs;
+        const int rr = lane >> 1, comp = lane & 1;
+        double v = 0.0;
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        a0r += __shfl_xor_sync(0xffffffffu, a0r, o);
-        a0i += __shfl_xor_sync(0xffffffffu, a0i, o);
-        a1r += __shfl_xor_sync(0xffffffffu, a1r, o);
-        a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
-      }
-      if (sd) {  // rows and reactions of a diagonal block share the slots: add the rows into s_re
-        __syncwarp();
-        if (ph == 0) {
-          if (v0) s_re[row0] = make_double2(s_re[row0].x + a0r, s_re[row0].y + a0i);
-          if (v1) s_re[row1] = make_double2(s_re[row1].x + a1r, s_re[row1].y + a1i);
+        for (int k = 0; k < 8; ++k) v += sd_[(k * 8 + rr) * 2 + comp];
+        const int row = rc + (rr & 3) + 4 * (rr >> 2);
+        if (row < tk.w) {
+          if (sd) {  // rows and reactions of a diagonal block share the slots: add into s_re
+            double* re_ = (double*)(s_re + row) + comp;
+            *re_ += v;
+          } else if (write_rows) {
+            ((double*)(part + (int64_t)(tb + row) * nslot + q))[comp] = v;
+          }
         }
-        __syncwarp();
-      } else if (ph == 0 && write_rows) {
-        if (v0) part[(int64_t)(tb + row0) * nslot + q] = make_double2(a0r, a0i);
-        if (v1) part[(int64_t)(tb + row1) * nslot + q] = make_double2(a1r, a1i);
       }
+      __syncwarp();
     }
     __syncwarp();
     if (whole && write_react)
