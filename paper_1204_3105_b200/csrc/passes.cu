@@ -265,100 +265,113 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
+// shared memory of one k_down_mma block (dynamic): P2P log / atan tables (b_0's Log), the
+// binomial A fragments, then per warp: powers, a~, Log, L2L part, Q, source ids
 template <int P>
-__global__ void __launch_bounds__(128) k_down_mma(int l, int B, int64_t ncells, int64_t span_l,
-                                                  const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
-                                                  const double2* __restrict__ cen_l,
-                                                  const double2* __restrict__ cen_par,
-                                                  const double2* __restrict__ loc_par,
-                                                  const int32_t* __restrict__ cand,
-                                                  const unsigned long long* __restrict__ e4mask,
-                                                  const double2* __restrict__ mp_l, int p,
-                                                  const double* __restrict__ binom, double2* __restrict__ loc_l) {
-  constexpr int NB = 8;             // sources per batch (2 n-tiles of 4 complex columns)
-  constexpr int MT = (P + 8) / 8;   // m-tiles over l = 0..P
-  constexpr int KT = P / 4;         // k-tiles over k = 1..P
-  __shared__ double2 s_pw[4][NB][P + 1];  // w_s^k
-  __shared__ double2 s_at[4][NB][P];      // a~_{s,k}, k = 1..P
-  __shared__ double2 s_lg[4][NB];
-  __shared__ double s_q[4][NB];
-  __shared__ int s_src[4][NB];
-  __shared__ double2 s_b[4][32];          // L2L part
+struct DownSmem {
+  static constexpr int NB = 8, MT = (P + 8) / 8, KT = P / 4;
+  static constexpr size_t tab = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1));
+  static constexpr size_t afr = sizeof(double) * MT * KT * 32;
+  static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + NB + 32) + sizeof(double) * NB +
+                                 sizeof(int) * FMM_CAND_MAX;
+  static constexpr size_t bytes = tab + afr + 4 * warp;
+};
+
+#ifndef DOWN_MINB
+#define DOWN_MINB(P) ((P) >= 20 ? 4 : 5)  // resident blocks per SM (register budget 128 / 96)
+#endif
+template <int P>
+__global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, int64_t ncells, int64_t span_l,
+                                                     const int32_t* __restrict__ toff, int64_t leaf_lo,
+                                                     int64_t leaf_hi, const double2* __restrict__ cen_l,
+                                                     const double2* __restrict__ cen_par,
+                                                     const double2* __restrict__ loc_par,
+                                                     const int32_t* __restrict__ cand,
+                                                     const unsigned long long* __restrict__ e4mask,
+                                                     const double2* __restrict__ mp_l, int p,
+                                                     const double* __restrict__ binom, const double* __restrict__ tabs,
+                                                     double2* __restrict__ loc_l) {
+  using S = DownSmem<P>;
+  constexpr int NB = S::NB, MT = S::MT, KT = S::KT;
+  extern __shared__ double2 dsm[];
+  double2* s_log = dsm;
+  double2* s_atan = s_log + P2P_LOG_N;
+  double* s_afr = (double*)((char*)dsm + S::tab);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  char* wb = (char*)dsm + S::tab + S::afr + w * S::warp;
+  double2* s_pw = (double2*)wb;          // [NB][P+1] w_s^k
+  double2* s_at = s_pw + NB * (P + 1);   // [NB][P]   a~_{s,k}, k = 1..P
+  double2* s_lg = s_at + NB * P;         // [NB]      Log(c_t - c_s)
+  double2* s_b = s_lg + NB;              // [32]      L2L part
+  double* s_q = (double*)(s_b + 32);     // [NB]
+  int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
+  p2p_load_tables(tabs, s_log, s_atan);  // ends with __syncthreads
+  // A fragments: Cb[r][k] = C(r+k-1, k-1), row r = 8 mt + ln/4, column k = 4 kt + ln%4 + 1
+  for (int i = threadIdx.x; i < MT * KT * 32; i += blockDim.x) {
+    const int ln = i & 31, kt = (i >> 5) % KT, mt = (i >> 5) / KT;
+    const int r = 8 * mt + (ln >> 2), k = 4 * kt + (ln & 3) + 1;
+    s_afr[i] = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
+  }
+  __syncthreads();
+  const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
   if (t >= ncells) return;
   const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
   if (thi <= tlo || toff[thi] == toff[tlo]) return;  // no targets of this rank below t
   const double2 ct = cen_l[t];
   const int64_t par = t / B;
+  // ---- E4(t) source ids, ascending: lane i places candidates i and i + 32 by prefix popcount
+  const unsigned long long mask = e4mask[t];
+  const int32_t* cd = cand + par * FMM_CAND_MAX;
+  {
+    const unsigned lo = (unsigned)mask, hi = (unsigned)(mask >> 32), below = (1u << lane) - 1u;
+    if ((lo >> lane) & 1u) s_src[__popc(lo & below)] = cd[lane];
+    if ((hi >> lane) & 1u) s_src[__popc(lo) + __popc(hi & below)] = cd[lane + 32];
+  }
+  const int nsrc = __popcll(mask);
   // ---- L2L (lane = coefficient): Horner in w = c_t - c_par over k = p..l
   {
     double2 acc = make_double2(0.0, 0.0);
     if (l >= 2) {
       const double2 cpp = cen_par[par];
       const double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
-      s_b[w][lane] = lane <= p ? loc_par[par * (p + 1) + lane] : make_double2(0.0, 0.0);
+      s_b[lane] = lane <= p ? loc_par[par * (p + 1) + lane] : make_double2(0.0, 0.0);
       __syncwarp();
       for (int k = p; k >= 0; --k) {
-        const double2 bk = s_b[w][k];
+        const double2 bk = s_b[k];
         if (k >= lane && lane <= p) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + lane], bk));
       }
       __syncwarp();
     }
-    s_b[w][lane] = acc;
-  }
-  // ---- A fragments: Cb[l][k] = C(l+k-1, k-1), row l = 8 mt + lane/4, column k = 4 kt + lane%4 + 1
-  double afr[MT][KT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt) {
-      const int r = 8 * mt + (lane >> 2), k = 4 * kt + (lane & 3) + 1;
-      afr[mt][kt] = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
-    }
-  double inv_r[MT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int r = 8 * mt + (lane >> 2);
-    inv_r[mt] = r > 0 ? 1.0 / r : 0.0;
+    s_b[lane] = acc;
   }
   double2 acc[MT];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt] = make_double2(0.0, 0.0);
-  unsigned long long mask = e4mask[t];
-  const int32_t* cd = cand + par * FMM_CAND_MAX;
-  while (mask) {
-    int nb = 0;
-    {
-      unsigned long long mm = mask;
-      for (int j = 0; j < NB && mm; ++j) {
-        const int i = __ffsll((long long)mm) - 1;
-        mm &= mm - 1;
-        if (lane == 0) s_src[w][j] = cd[i];
-        ++nb;
-      }
-      mask = mm;
-    }
-    __syncwarp();
+  __syncwarp();
+  for (int b0 = 0; b0 < nsrc; b0 += NB) {
+    const int nb = min(NB, nsrc - b0);
     // powers: lane = (source s = lane / 4, residue j = lane % 4): w^(4m + j), m = 0..P/4
     {
       const int s = lane >> 2, j = lane & 3;
       if (s < nb) {
-        const double2 cs = cen_l[s_src[w][s]];
+        const int src = s_src[b0 + s];
+        const double2 cs = cen_l[src];
         const double zx = cs.x - ct.x, zy = cs.y - ct.y;
-        const double d = 1.0 / (zx * zx + zy * zy);
+        const double d = p2p_rcp(fma(zx, zx, zy * zy));
         const double2 wv = make_double2(zx * d, -zy * d);
         const double2 w2 = cmul(wv, wv);
         const double2 w4 = cmul(w2, w2);
         double2 pw = j == 0 ? make_double2(1.0, 0.0) : (j == 1 ? wv : (j == 2 ? w2 : cmul(w2, wv)));
 #pragma unroll
         for (int m = 0; 4 * m + j <= P && m <= P / 4; ++m) {
-          if (4 * m + j <= P) s_pw[w][s][4 * m + j] = pw;
+          if (4 * m + j <= P) s_pw[s * (P + 1) + 4 * m + j] = pw;
           pw = cmul(pw, w4);
         }
-        if (j == 0) {
-          s_lg[w][s] = clog_principal(ct.x - cs.x, ct.y - cs.y);  // Log(c_L - c_M), D13 (iii)
-          s_q[w][s] = mp_l[(int64_t)s_src[w][s] * (p + 1)].x;
+        if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
+          const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
+          s_lg[s] = make_double2(0.5 * p2p_log(fma(dx, dx, dy * dy), a_log), p2p_atan2(dy, dx, a_atan));
+          s_q[s] = mp_l[(int64_t)src * (p + 1)].x;
         }
       }
     }
@@ -368,15 +381,16 @@ __global__ void __launch_bounds__(128) k_down_mma(int l, int B, int64_t ncells, 
       const int s = idx / P, kk = idx % P, k = kk + 1;
       double2 v = make_double2(0.0, 0.0);
       if (s < nb && k <= p) {
-        const double2 a = mp_l[(int64_t)s_src[w][s] * (p + 1) + k];
-        v = cmul(a, s_pw[w][s][k]);
+        const double2 a = mp_l[(int64_t)s_src[b0 + s] * (p + 1) + k];
+        v = cmul(a, s_pw[s * (P + 1) + k]);
         if (k & 1) v = make_double2(-v.x, -v.y);
       }
-      s_at[w][s][kk] = v;
+      s_at[s * P + kk] = v;
     }
     __syncwarp();
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
+      if (4 * nt >= nb) break;
       double d[MT][2];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) d[mt][0] = d[mt][1] = 0.0;
@@ -384,26 +398,26 @@ __global__ void __launch_bounds__(128) k_down_mma(int l, int B, int64_t ncells, 
       const int bs = 4 * nt + (lane >> 3), bc = (lane >> 2) & 1;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
-        const double2 v = s_at[w][bs][4 * kt + (lane & 3)];
+        const double2 v = s_at[bs * P + 4 * kt + (lane & 3)];
         const double bfr = bc ? v.y : v.x;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma884(d[mt][0], d[mt][1], afr[mt][kt], bfr);
+        for (int mt = 0; mt < MT; ++mt) dmma884(d[mt][0], d[mt][1], s_afr[(mt * KT + kt) * 32 + lane], bfr);
       }
       // C[r][2c + {0,1}] at lane 4r + c: row r = l, source s = 4 nt + lane % 4 (re, im)
       const int s = 4 * nt + (lane & 3);
       if (s < nb) {
-        const double Q = s_q[w][s];
+        const double Q = s_q[s];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int r = 8 * mt + (lane >> 2);
           if (r > P) continue;
           if (r == 0) {
-            const double2 lg = s_lg[w][s];
+            const double2 lg = s_lg[s];
             acc[mt].x += Q * lg.x + d[mt][0];
             acc[mt].y += Q * lg.y + d[mt][1];
           } else {
-            const double2 pw = s_pw[w][s][r];
-            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, inv_r[mt], d[mt][0]), d[mt][1])));
+            const double2 pw = s_pw[s * (P + 1) + r];
+            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, 1.0 / r, d[mt][0]), d[mt][1])));
           }
         }
       }
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(128) k_down_mma(int l, int B, int64_t ncells, 
     acc[mt].x += __shfl_xor_sync(0xffffffffu, acc[mt].x, 2);
     acc[mt].y += __shfl_xor_sync(0xffffffffu, acc[mt].y, 2);
     const int r = 8 * mt + (lane >> 2);
-    if ((lane & 3) == 0 && r <= p) loc_l[t * (p + 1) + r] = cadd(acc[mt], s_b[w][r]);
+    if ((lane & 3) == 0 && r <= p) loc_l[t * (p + 1) + r] = cadd(acc[mt], s_b[r]);
   }
 }
 
@@ -429,10 +443,16 @@ static void launch_down(fmm_tree_s* t, int l) {
   const int64_t nc = G.ncells[l];
   static const bool simt = getenv("FMM_M2L_SIMT") && getenv("FMM_M2L_SIMT")[0] == '1';
   if (!simt) {
-    k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_down_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DownSmem<P>::bytes);
+      attr = true;
+    }
+    k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, DownSmem<P>::bytes, t->stream>>>(
         l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
-        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
+        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->p2p_tab,
+        t->loc + G.lvl_off[l] * (p + 1));
     return;
   }
   k_down2<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
