@@ -271,7 +271,7 @@ template <int P>
 struct DownSmem {
   static constexpr int NB = 8, MT = (P + 8) / 8, KT = P / 4;
   static constexpr size_t tab = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1));
-  static constexpr size_t afr = sizeof(double) * MT * KT * 32;
+  static constexpr size_t afr = sizeof(double) * (MT * KT * 32 + 8 * MT);  // + 1/r table
   static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + NB + 32) + sizeof(double) * NB +
                                  sizeof(int) * FMM_CAND_MAX;
   static constexpr size_t bytes = tab + afr + 4 * warp;
@@ -312,6 +312,8 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
     const int r = 8 * mt + (ln >> 2), k = 4 * kt + (ln & 3) + 1;
     s_afr[i] = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
   }
+  double* s_invr = s_afr + MT * KT * 32;  // [8 MT] 1/r (0 for r = 0)
+  for (int i = threadIdx.x; i < 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
   __syncthreads();
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -376,16 +378,23 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
       }
     }
     __syncwarp();
-    // a~_{s,k} = (-1)^k a_{s,k} w_s^k
-    for (int idx = lane; idx < NB * P; idx += 32) {
-      const int s = idx / P, kk = idx % P, k = kk + 1;
-      double2 v = make_double2(0.0, 0.0);
-      if (s < nb && k <= p) {
-        const double2 a = mp_l[(int64_t)s_src[b0 + s] * (p + 1) + k];
-        v = cmul(a, s_pw[s * (P + 1) + k]);
-        if (k & 1) v = make_double2(-v.x, -v.y);
+    // a~_{s,k} = (-1)^k a_{s,k} w_s^k: all loads of the batch first, then the products
+    static_assert((NB * P) % 32 == 0, "a~ staging assumes whole warp rounds");
+    constexpr int NR = NB * P / 32;
+    {
+      double2 av[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int idx = lane + 32 * i, s = idx / P, k = idx % P + 1;
+        av[i] = (s < nb && k <= p) ? mp_l[(int64_t)s_src[b0 + s] * (p + 1) + k] : make_double2(0.0, 0.0);
       }
-      s_at[s * P + kk] = v;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int idx = lane + 32 * i, s = idx / P, k = idx % P + 1;
+        double2 v = cmul(av[i], s_pw[s * (P + 1) + k]);
+        if (k & 1) v = make_double2(-v.x, -v.y);
+        s_at[idx] = v;  // = s_at[s * P + k - 1]
+      }
     }
     __syncwarp();
 #pragma unroll
@@ -417,7 +426,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
             acc[mt].y += Q * lg.y + d[mt][1];
           } else {
             const double2 pw = s_pw[s * (P + 1) + r];
-            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, 1.0 / r, d[mt][0]), d[mt][1])));
+            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, s_invr[r], d[mt][0]), d[mt][1])));
           }
         }
       }
