@@ -337,15 +337,25 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   carve(t, a);
   t->slab = slab;
   t->slab_bytes = sizer.off;
-  static std::vector<double> hb = host_binom();
-  static std::vector<double> htab = [] {
-    std::vector<double> v(P2P_TAB_DOUBLES);
-    fmm_host_p2p_tables(v.data());
-    return v;
-  }();
-  ce = cudaMemcpyAsync(t->binom, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+  // binomials and P2P tables: one pinned host copy per process, so that these copies stay
+  // asynchronous (a pageable source would synchronise the stream with the host)
+  static double* hconst = nullptr;
+  static cudaError_t hconst_err = cudaSuccess;
+  static std::once_flag hconst_once;
+  std::call_once(hconst_once, [] {
+    const size_t nb = (size_t)BS * BS;
+    hconst_err = cudaHostAlloc((void**)&hconst, (nb + P2P_TAB_DOUBLES) * sizeof(double), cudaHostAllocPortable);
+    if (hconst_err != cudaSuccess) return;
+    std::vector<double> hb = host_binom();
+    memcpy(hconst, hb.data(), nb * sizeof(double));
+    fmm_host_p2p_tables(hconst + nb);
+  });
+  ce = hconst_err;
   if (ce == cudaSuccess)
-    ce = cudaMemcpyAsync(t->p2p_tab, htab.data(), htab.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+    ce = cudaMemcpyAsync(t->binom, hconst, (size_t)BS * BS * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(t->p2p_tab, hconst + (size_t)BS * BS, P2P_TAB_DOUBLES * sizeof(double),
+                         cudaMemcpyHostToDevice, s);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(t->status, 0xff, sizeof(DevStatus), s);
   if (ce != cudaSuccess) {
     fmm_set_error_message(cudaGetErrorString(ce));
