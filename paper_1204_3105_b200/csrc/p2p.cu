@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
 
 // ------------------------------------------------------------------ partial sums + L2P -> Phi
 // one warp per target leaf; lanes over its targets; slots added in near-list order
+template <int NS>  // slots per target (nslot): all loads of a target issued together
 __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, const int32_t* __restrict__ toff,
                                                     const int32_t* __restrict__ nnear, const double2* __restrict__ txy,
                                                     const double2* __restrict__ cen_leaf,
@@ -349,11 +350,14 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
   const double2* b = loc_leaf + t * (p + 1);
   for (int i = lane; i < nt; i += 32) {
     const int tpos = tb + i;
+    double2 v[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) v[q] = q < nn ? part[(int64_t)tpos * nslot + q] : make_double2(0.0, 0.0);
     double re = 0.0, im = 0.0;
-    for (int q = 0; q < nn; ++q) {
-      const double2 v = part[(int64_t)tpos * nslot + q];
-      re += v.x;
-      im += v.y;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {  // near-list order
+      re += v[q].x;
+      im += v[q].y;
     }
     const double2 y = txy[tpos];
     const double2 z = make_double2(y.x - c.x, y.y - c.y);
@@ -411,9 +415,19 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   if (t->timing) cudaEventRecord(t->ev[7], s);
   const int64_t nl = t->leaf_hi - t->leaf_lo;
   if (nl > 0)
-    k_p2p_finish<<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(
-        t->leaf_lo, t->leaf_hi, t->toff, t->nnear, t->txy, t->centre + G.lvl_off[G.L],
-        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, G.nslot, phi);
+    switch (G.nslot) {
+#define FMM_FINISH(NS)                                                                                        \
+  case NS:                                                                                                    \
+    k_p2p_finish<NS><<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(                                       \
+        t->leaf_lo, t->leaf_hi, t->toff, t->nnear, t->txy, t->centre + G.lvl_off[G.L],                        \
+        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, G.nslot, phi);                             \
+    break;
+      FMM_FINISH(7)
+      FMM_FINISH(9)
+      FMM_FINISH(13)
+#undef FMM_FINISH
+      default: return FMM_EBADCFG;
+    }
   t->launches += 2;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
