@@ -11,6 +11,8 @@
 // one-sided blocks.  Every (target, near-leaf) pair of the near list owns one partial-sum
 // slot written by exactly one task in a fixed order, and a final pass adds the slots in
 // near-list order, so the result is deterministic.
+#include <type_traits>
+
 #include "fmm_internal.cuh"
 #include "p2p_math.cuh"
 
@@ -113,7 +115,7 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 #define P2P_WARPS 8  // warps per block (the tables are shared by the block)
 #endif
 #ifndef P2P_MINB
-#define P2P_MINB 3  // resident blocks per SM the register allocation is sized for
+#define P2P_MINB 2  // resident blocks per SM the register allocation is sized for (128 registers)
 #endif
 constexpr int P2P_RS = 32;  // row stride (double2) of the reaction scratch; column c of row lane r sits at c ^ 2r
                             // (conflict-free STS.128 / LDS.128)
@@ -242,31 +244,59 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
           const bool react = sym && !(sd && a <= rc + 7);
           const bool two = cnt - 16 * h > 8;  // ... and an empty last quarter
           double vr[2] = {0.0, 0.0}, vi[2] = {0.0, 0.0};
+          // NJ columns x 2 rows in one basic block (the slow-path test covers all of them), so
+          // that the compiler overlaps the 2 NJ independent pairs
+          auto cols = [&](auto njc) {
+            constexpr int NJ = decltype(njc)::value;
+            double2 x[NJ];
+            double uc[NJ], dx[NJ][2], dy[NJ][2], r2[NJ][2];
+            PairOut pr[NJ][2];
+            bool slow = false;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j == 1 && !two) break;
-            const int k = 16 * h + 8 * j + ph;
-            const double2 x = s_xy[cb + k];
-            const double uc = s_u[cb + k];
-            const int col = c0 + k;
-            const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
-            const double dx0 = y0.x - x.x, dy0 = y0.y - x.y, dx1 = y1.x - x.x, dy1 = y1.y - x.y;
-            const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
-            PairOut p0 = p2p_fast(dx0, dy0, r20, a_log, a_atan);
-            PairOut p1 = p2p_fast(dx1, dy1, r21, a_log, a_atan);
-            const bool sl0 = __double2hiint(r20) < P2P_SLOW_HI, sl1 = __double2hiint(r21) < P2P_SLOW_HI;
-            if (__builtin_expect(sl0 || sl1, 0)) {
-              if (sl0) p0 = p2p_slow(dx0, dy0, r20, diag && col == row0, tperm, tb + row0, scol, st);
-              if (sl1) p1 = p2p_slow(dx1, dy1, r21, diag && col == row1, tperm, tb + row1, scol, st);
+            for (int j = 0; j < NJ; ++j) {
+              const int k = 16 * h + 8 * j + ph;
+              x[j] = s_xy[cb + k];
+              uc[j] = s_u[cb + k];
+              dx[j][0] = y0.x - x[j].x;
+              dy[j][0] = y0.y - x[j].y;
+              dx[j][1] = y1.x - x[j].x;
+              dy[j][1] = y1.y - x[j].y;
+#pragma unroll
+              for (int r = 0; r < 2; ++r) {
+                r2[j][r] = fma(dx[j][r], dx[j][r], dy[j][r] * dy[j][r]);
+                pr[j][r] = p2p_fast(dx[j][r], dy[j][r], r2[j][r], a_log, a_atan);
+                slow |= __double2hiint(r2[j][r]) < P2P_SLOW_HI;
+              }
             }
-            a0r = fma(uc, p0.lg, a0r);
-            a0i = fma(uc, p0.ag, a0i);
-            a1r = fma(uc, p1.lg, a1r);
-            a1i = fma(uc, p1.ag, a1i);
-            // reversed pairs: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
-            vr[j] = fma(u0, p0.lg, u1 * p1.lg);
-            vi[j] = fma(u0, p0.ag > 0.0 ? p0.ag - PI : p0.ag + PI, u1 * (p1.ag > 0.0 ? p1.ag - PI : p1.ag + PI));
-          }
+            if (__builtin_expect(slow, 0)) {
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                const int col = c0 + 16 * h + 8 * j + ph;
+                const int scol = sym ? sb + col : -1;  // self mode: the column is a target too
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                  const int row = r ? row1 : row0;
+                  if (__double2hiint(r2[j][r]) < P2P_SLOW_HI)
+                    pr[j][r] = p2p_slow(dx[j][r], dy[j][r], r2[j][r], diag && col == row, tperm, tb + row, scol, st);
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              a0r = fma(uc[j], pr[j][0].lg, a0r);
+              a0i = fma(uc[j], pr[j][0].ag, a0i);
+              a1r = fma(uc[j], pr[j][1].lg, a1r);
+              a1i = fma(uc[j], pr[j][1].ag, a1i);
+              // reversed pairs: same log|z|^2, Arg(-z) = Arg z - pi (Arg z > 0) or + pi (Arg z <= 0)
+              const double g0 = pr[j][0].ag, g1 = pr[j][1].ag;
+              vr[j] = fma(u0, pr[j][0].lg, u1 * pr[j][1].lg);
+              vi[j] = fma(u0, g0 > 0.0 ? g0 - PI : g0 + PI, u1 * (g1 > 0.0 ? g1 - PI : g1 + PI));
+            }
+          };
+          if (two)
+            cols(std::integral_constant<int, 2>{});
+          else
+            cols(std::integral_constant<int, 1>{});
           if (react) {  // the 4 row lanes' partials of the 2 columns, summed below
             s_rs[tl * P2P_RS + ((16 * h + ph) ^ (2 * tl))] = make_double2(vr[0], vi[0]);
             s_rs[tl * P2P_RS + ((16 * h + 8 + ph) ^ (2 * tl))] = make_double2(vr[1], vi[1]);
