@@ -256,19 +256,19 @@ __global__ void k_cand_level(DGeo g, int l, const int32_t* __restrict__ soff, co
     return;
   }
   int32_t* my = cand + P * FMM_CAND_MAX;
-  int64_t pn[16];
+  // {P} U Neighbors(P) sorted (<= 13 cells); their children occupy disjoint ascending key
+  // ranges [Q B, Q B + B), so emitting children in that order gives the ascending candidates
+  int64_t pn[17];
   int npn = geo_neighbors(g, l - 1, P, pn);
-  int64_t c[FMM_CAND_MAX];
+  pn[npn++] = P;
+  sort_small(pn, npn);
   int nc = 0;
-  for (int q = -1; q < npn; ++q) {
-    int64_t Q = q < 0 ? P : pn[q];
+  for (int q = 0; q < npn; ++q) {
     for (int ch = 0; ch < B; ++ch) {
-      int64_t cc = Q * B + ch;
-      if (cell_count(soff, cc, span_l) > 0) c[nc++] = cc;
+      int64_t cc = pn[q] * B + ch;
+      if (cell_count(soff, cc, span_l) > 0) my[nc++] = (int32_t)cc;
     }
   }
-  sort_small(c, nc);
-  for (int i = 0; i < nc; ++i) my[i] = (int32_t)c[i];
   ncand[P] = nc;
 }
 

@@ -79,20 +79,25 @@ __device__ inline int quad_neighbors(int l, int64_t n, int64_t* out) {
 
 // ------------------------------------------------------------------ septree (integer lattice)
 // unit digit d -> lattice step on the (digit-1 at 30 deg, digit-2 at 90 deg) basis (D3, D5)
+//   UB = {0, 1, 0, -1, -1, 0, 1}, UC = {0, 0, 1, 1, 0, -1, -1}, packed as 2-bit (v + 1) fields
 __host__ __device__ inline void sept_unit(int d, int64_t* b, int64_t* c) {
-  const int UB[7] = {0, 1, 0, -1, -1, 0, 1};
-  const int UC[7] = {0, 0, 1, 1, 0, -1, -1};
-  *b = UB[d];
-  *c = UC[d];
+  *b = (int64_t)((0x2419u >> (2 * d)) & 3u) - 1;
+  *c = (int64_t)((0x1a5u >> (2 * d)) & 3u) - 1;
 }
 // address (l digits, MSB first) -> lattice coordinates of the level-l lattice: Horner with
 // lambda, v <- M v + unit(t_i), M(b, c) = (b - 2c, 2b + 3c)
 __host__ __device__ inline void sept_addr_to_lattice(int64_t n, int l, int64_t* b, int64_t* c) {
-  int64_t B = 0, C = 0;
-  int64_t pw = ipow_d(7, l - 1);
+  // digits LSB first by constant division (n < 7^10 < 2^32), packed 3 bits each, then Horner
+  // from the most significant digit
+  uint32_t m = (uint32_t)n;
+  uint64_t packed = 0;
   for (int i = 0; i < l; ++i) {
-    int d = (int)((n / pw) % 7);
-    pw /= 7;
+    packed |= (uint64_t)(m % 7u) << (3 * i);
+    m /= 7u;
+  }
+  int64_t B = 0, C = 0;
+  for (int i = l - 1; i >= 0; --i) {
+    const int d = (int)((packed >> (3 * i)) & 7u);
     int64_t nb = B - 2 * C, nc = 2 * B + 3 * C;
     int64_t ub, uc;
     sept_unit(d, &ub, &uc);
@@ -112,18 +117,26 @@ __host__ __device__ inline void sept_lambda_pow(int k, int64_t* b, int64_t* c) {
 }
 // lattice -> address with at most maxd digits (false if more are needed): digit extraction
 // d = T[(b + 3c) mod 7], (b, c) <- M^-1((b, c) - unit(d)), M^-1 = [[3, 2], [-2, 1]] / 7
-__host__ __device__ inline bool sept_lattice_to_addr(int64_t b, int64_t c, int maxd, int64_t* n) {
-  const int T[7] = {0, 1, 3, 2, 5, 6, 4};
+__host__ __device__ inline bool sept_lattice_to_addr(int64_t b64, int64_t c64, int maxd, int64_t* n) {
+  // an address of <= 10 digits has |b|, |c| < 7^5 * 3 (far below 2^27): larger lattice
+  // points are out of the domain, and the rest fits 32-bit arithmetic (exact /7 by the
+  // modular inverse 0xB6DB6DB7 of 7 mod 2^32, since the differences below are multiples of 7)
+  if (b64 <= -(1 << 27) || b64 >= (1 << 27) || c64 <= -(1 << 27) || c64 >= (1 << 27)) return false;
+  // T = {0, 1, 3, 2, 5, 6, 4} as nibbles (no local-memory table)
+  constexpr uint32_t T = 0x4652310u;
+  int32_t b = (int32_t)b64, c = (int32_t)c64;
   int64_t key = 0, pw = 1;
   for (int k = 0; k < maxd; ++k) {
     if (b == 0 && c == 0) break;
-    int r = (int)(((b + 3 * c) % 7 + 7) % 7);
-    int d = T[r];
+    int r = (b + 3 * c) % 7;
+    if (r < 0) r += 7;
+    const int d = (int)((T >> (4 * r)) & 7u);
     int64_t ub, uc;
     sept_unit(d, &ub, &uc);
-    b -= ub;
-    c -= uc;
-    int64_t nb = (3 * b + 2 * c) / 7, nc = (-2 * b + c) / 7;
+    b -= (int32_t)ub;
+    c -= (int32_t)uc;
+    const int32_t nb = (int32_t)((uint32_t)(3 * b + 2 * c) * 0xB6DB6DB7u);
+    const int32_t nc = (int32_t)((uint32_t)(-2 * b + c) * 0xB6DB6DB7u);
     b = nb;
     c = nc;
     key += d * pw;
@@ -139,23 +152,23 @@ __device__ inline bool sept_key(const DGeo& g, double x, double y, uint32_t* key
   double b = __ddiv_rn(__dmul_rn(2.0, xp), g.sept_D3r);                  // eq. P:212
   double c = __ddiv_rn(__dsub_rn(__dmul_rn(yp, FMM_S3), xp), g.sept_D3r);
   if (!(fabs(b) < 1.0e9) || !(fabs(c) < 1.0e9)) return false;
-  double bf = floor(b), bc = ceil(b), cf = floor(c), cc = ceil(c);     // eq. P:237 order
-  double cb[4] = {bf, bc, bf, bc}, ccand[4] = {cf, cf, cc, cc};
-  int best = 0;
-  double bestd = 0.0;
+  const double bf = floor(b), bc = ceil(b), cf = floor(c), cc = ceil(c);  // eq. P:237 order
+  double bb = bf, bcc = cf, bestd = 0.0;  // best candidate (first wins ties)
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    double lx = __dmul_rn(g.sept_A, cb[q]);                               // eq. P:230
-    double ly = __dmul_rn(g.sept_Bc, __dadd_rn(__dmul_rn(2.0, ccand[q]), cb[q]));
+    const double qb = (q & 1) ? bc : bf, qc = (q & 2) ? cc : cf;  // (bf,cf) (bc,cf) (bf,cc) (bc,cc)
+    double lx = __dmul_rn(g.sept_A, qb);                                  // eq. P:230
+    double ly = __dmul_rn(g.sept_Bc, __dadd_rn(__dmul_rn(2.0, qc), qb));
     double dx = __dsub_rn(xp, lx), dy = __dsub_rn(yp, ly);
     double d = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
     if (q == 0 || d < bestd) {
-      best = q;
+      bb = qb;
+      bcc = qc;
       bestd = d;
     }
   }
   int64_t n;
-  if (!sept_lattice_to_addr((int64_t)cb[best], (int64_t)ccand[best], g.L, &n)) return false;
+  if (!sept_lattice_to_addr((int64_t)bb, (int64_t)bcc, g.L, &n)) return false;
   *key = (uint32_t)n;
   return true;
 }
@@ -193,24 +206,29 @@ __device__ inline bool triq_key(const DGeo& g, double x, double y, uint32_t* key
   double u = 0.0, v = 0.0;
   double up = 1.0;
   uint32_t t = 0;
+  double Ri = R0;
   for (int i = 1; i <= g.L; ++i) {
-    double Ri = ldexp(R0, -i), RH = __dmul_rn(Ri, FMM_H), half = 0.5 * Ri;
+    Ri = 0.5 * Ri;  // = R0 2^-i exactly (as ldexp)
+    double RH = __dmul_rn(Ri, FMM_H), half = 0.5 * Ri;
     double su = up * Ri, sh = up * half;  // exact
-    double cu[4] = {u, u, __dsub_rn(u, RH), __dadd_rn(u, RH)};
-    double cv[4] = {v, __dadd_rn(v, su), __dsub_rn(v, sh), __dsub_rn(v, sh)};
+    const double vs = __dsub_rn(v, sh);
     int best = 0;
-    double bestd = 0.0;
+    double bestd = 0.0, bu = u, bv = v;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      double dx = __dsub_rn(xp, cu[q]), dy = __dsub_rn(yp, cv[q]);
+      const double cu = q < 2 ? u : (q == 2 ? __dsub_rn(u, RH) : __dadd_rn(u, RH));
+      const double cv = q == 0 ? v : (q == 1 ? __dadd_rn(v, su) : vs);
+      double dx = __dsub_rn(xp, cu), dy = __dsub_rn(yp, cv);
       double d = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
       if (q == 0 || d < bestd) {
         best = q;
         bestd = d;
+        bu = cu;
+        bv = cv;
       }
     }
-    u = cu[best];
-    v = cv[best];
+    u = bu;
+    v = bv;
     if (best == 0) up = -up;  // centre child: orientation flips
     t = t * 4 + best;
   }
@@ -239,14 +257,15 @@ __device__ inline double2 triq_centre(const DGeo& g, int l, int64_t n) {
 
 // adjacentNeighbor by ancestor-sibling-reflect with Table 1; k: 0 L, 1 R, 2 V
 __device__ inline int64_t triq_adjacent(int l, int64_t n, int k) {
-  // Table 1 packed: D[type][k] and star flags
-  const int D[4][3] = {{2, 3, 1}, {3, 2, 0}, {1, 0, 2}, {0, 1, 3}};
-  const int STAR[4][3] = {{1, 1, 1}, {0, 0, 1}, {0, 1, 0}, {1, 0, 0}};
+  // Table 1 packed into constants (no local-memory tables):
+  //   D[type][k] = {{2, 3, 1}, {3, 2, 0}, {1, 0, 2}, {0, 1, 3}}     2 bits at 2 (3 type + k)
+  //   STAR[type][k] = {{1, 1, 1}, {0, 0, 1}, {0, 1, 0}, {1, 0, 0}}  1 bit at 3 type + k
+  constexpr uint32_t DP = 0xd212deu, SP = 0x2a7u;
   if (n < 0) return -1;
   int i = l;  // digit position from the right end
   while (i >= 1) {
     int d = (int)((n >> (2 * (l - i))) & 3);
-    if (STAR[d][k]) break;
+    if ((SP >> (3 * d + k)) & 1u) break;
     --i;
   }
   if (i < 1) return -1;
@@ -254,7 +273,7 @@ __device__ inline int64_t triq_adjacent(int l, int64_t n, int k) {
   for (int j = i; j <= l; ++j) {
     int sh = 2 * (l - j);
     int d = (int)((n >> sh) & 3);
-    r = (r & ~((int64_t)3 << sh)) | ((int64_t)D[d][k] << sh);
+    r = (r & ~((int64_t)3 << sh)) | ((int64_t)((DP >> (2 * (3 * d + k))) & 3u) << sh);
   }
   return r;
 }
