@@ -19,7 +19,7 @@
 namespace {
 
 constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) block
-constexpr int P2P_S = 160;          // sources of one near leaf kept in shared memory per warp
+constexpr int P2P_S = 192;          // sources of one near leaf kept in shared memory per warp
 constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
