@@ -125,73 +125,85 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_apply(const int32_t* in, int64_
   }
 }
 
-// ------------------------------------------------------------------ LSD radix sort (8-bit digits)
-constexpr int RS_T = 256, RS_ROUNDS = 16, RS_TILE = RS_T * RS_ROUNDS;
+// ------------------------------------------------------------------ LSD radix sort (<= 10-bit digits)
+// A tile of RS_TILE keys is split into RS_W warp segments of RS_SEG consecutive keys.  Ranks are
+// stable: order = (warp segment, round, lane), from warp match masks and warp-private per-digit
+// counters, so each tile needs only two block barriers per pass.
+constexpr int RS_W = 8, RS_T = 32 * RS_W, RS_SEG = 512, RS_TILE = RS_W * RS_SEG, RS_MAXB = 10;
 
 __global__ void __launch_bounds__(RS_T) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                                          int32_t* __restrict__ tile_hist, int ntiles) {
-  __shared__ int cnt[256];
-  cnt[threadIdx.x] = 0;
+                                                          int db, int32_t* __restrict__ tile_hist, int ntiles) {
+  __shared__ int cnt[RS_W][1 << RS_MAXB];
+  const int nb = 1 << db, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int d = lane; d < nb; d += 32) cnt[w][d] = 0;
+  __syncwarp();
+  const int64_t seg0 = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * RS_SEG;
+  const unsigned mask = (unsigned)nb - 1u;
+  for (int r = 0; r < RS_SEG / 32; ++r) {
+    const int64_t i = seg0 + 32 * r + lane;
+    const bool valid = i < n;
+    const unsigned d = valid ? ((keys[i] >> shift) & mask) : (unsigned)(nb + lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (valid && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
+    __syncwarp();
+  }
   __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * RS_TILE;
-  for (int r = 0; r < RS_ROUNDS; ++r) {
-    int64_t i = base + r * RS_T + threadIdx.x;
-    if (i < n) {
-      unsigned d = (keys[i] >> shift) & 255u;
-      unsigned peers = __match_any_sync(__activemask(), d);
-      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[d], __popc(peers));
+  for (int d = threadIdx.x; d < nb; d += RS_T) {
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < RS_W; ++q) c += cnt[q][d];
+    tile_hist[(int64_t)d * ntiles + blockIdx.x] = c;
+  }
+}
+
+__global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __restrict__ keys,
+                                                            const int32_t* __restrict__ vals, int64_t n, int shift,
+                                                            int db, const int32_t* __restrict__ tile_off, int ntiles,
+                                                            uint32_t* __restrict__ keys_out,
+                                                            int32_t* __restrict__ vals_out) {
+  __shared__ int wb[RS_W][1 << RS_MAXB];  // per warp and digit: count, then running output position
+  const int nb = 1 << db, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned mask = (unsigned)nb - 1u, lt = (1u << lane) - 1u;
+  for (int d = lane; d < nb; d += 32) wb[w][d] = 0;
+  __syncwarp();
+  const int64_t seg0 = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * RS_SEG;
+  // 1. per-warp digit counts of the warp's segment
+  for (int r = 0; r < RS_SEG / 32; ++r) {
+    const int64_t i = seg0 + 32 * r + lane;
+    const bool valid = i < n;
+    const unsigned d = valid ? ((keys[i] >> shift) & mask) : (unsigned)(nb + lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (valid && lane == __ffs(peers) - 1) wb[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // 2. output base of each (warp, digit): the tile's offset of the digit + earlier warps
+  for (int d = threadIdx.x; d < nb; d += RS_T) {
+    int run = tile_off[(int64_t)d * ntiles + blockIdx.x];
+#pragma unroll
+    for (int q = 0; q < RS_W; ++q) {
+      const int c = wb[q][d];
+      wb[q][d] = run;
+      run += c;
     }
   }
   __syncthreads();
-  tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
-}
-
-// stable scatter: element order within a tile = (round, warp, lane); ranks from warp
-// match masks plus a per-digit prefix over warps and rounds.
-__global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __restrict__ keys,
-                                                            const int32_t* __restrict__ vals, int64_t n, int shift,
-                                                            const int32_t* __restrict__ tile_off, int ntiles,
-                                                            uint32_t* __restrict__ keys_out,
-                                                            int32_t* __restrict__ vals_out) {
-  __shared__ int gofs[256];
-  __shared__ int base[256];
-  __shared__ int wcnt[RS_T / 32][256];
-  __shared__ int wpre[RS_T / 32][256];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  gofs[t] = tile_off[(int64_t)t * ntiles + blockIdx.x];
-  base[t] = 0;
-#pragma unroll
-  for (int q = 0; q < RS_T / 32; ++q) wcnt[q][t] = 0;
-  __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  int64_t tile0 = (int64_t)blockIdx.x * RS_TILE;
-  for (int r = 0; r < RS_ROUNDS; ++r) {
-    int64_t i = tile0 + r * RS_T + t;
-    bool valid = i < n;
-    uint32_t k = valid ? keys[i] : 0u;
-    int32_t v = valid ? (vals ? vals[i] : (int32_t)i) : 0;
-    unsigned d = valid ? ((k >> shift) & 255u) : (256u + lane);
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    int rank = __popc(peers & lt_mask);
-    if (valid && lane == __ffs(peers) - 1) wcnt[w][d] = __popc(peers);
-    __syncthreads();
-    {
-      int run = base[t];
-#pragma unroll
-      for (int q = 0; q < RS_T / 32; ++q) {
-        int c = wcnt[q][t];
-        wpre[q][t] = run;
-        wcnt[q][t] = 0;
-        run += c;
-      }
-      base[t] = run;
-    }
-    __syncthreads();
+  // 3. stable scatter in (round, lane) order within the warp's segment
+  for (int r = 0; r < RS_SEG / 32; ++r) {
+    const int64_t i = seg0 + 32 * r + lane;
+    const bool valid = i < n;
+    const uint32_t k = valid ? keys[i] : 0u;
+    const unsigned d = valid ? ((k >> shift) & mask) : (unsigned)(nb + lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    int pos = 0;
+    if (valid) pos = wb[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wb[w][d] += __popc(peers);
     if (valid) {
-      int pos = gofs[d] + wpre[w][d] + rank;
       keys_out[pos] = k;
-      vals_out[pos] = v;
+      vals_out[pos] = vals ? vals[i] : (int32_t)i;
     }
+    __syncwarp();
   }
 }
 
@@ -354,10 +366,10 @@ static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
 static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm) {
   if (n == 0) return FMM_OK;
   cudaStream_t s = t->stream;
-  int bits = key_bits(t->g.K);
-  int passes = (bits + 7) / 8;
-  int ntiles = (int)((n + RS_TILE - 1) / RS_TILE);
-  int64_t nhist = (int64_t)256 * ntiles;
+  const int bits = key_bits(t->g.K);
+  const int passes = (bits + RS_MAXB - 1) / RS_MAXB;
+  const int ntiles = (int)((n + RS_TILE - 1) / RS_TILE);
+  const int64_t nhist = ((int64_t)1 << ((bits + passes - 1) / passes)) * ntiles;
   // scratch: kA kB (n u32), vA (n i32), hist (nhist), scan scratch
   size_t need = (size_t)n * 4 * 3 + (size_t)nhist * 4 + fmm_scan_scratch_bytes(nhist) + 256;
   if (t->scratch_bytes < need) {
@@ -378,18 +390,23 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
   void* sscr = p;
   const uint32_t* kin = keys;
   const int32_t* vin = nullptr;  // iota on the first pass
+  int shift = 0;
   for (int ps = 0; ps < passes; ++ps) {
+    // balanced digit widths: the first (bits % passes) passes take one more bit
+    const int db = bits / passes + (ps < bits % passes ? 1 : 0);
+    const int64_t nh = ((int64_t)1 << db) * ntiles;
     uint32_t* kout = (ps % 2 == 0) ? kA : kB;
     // values alternate between vA and perm such that the last pass writes perm
     int32_t* vout = ((passes - 1 - ps) % 2 == 0) ? perm : vA;
-    k_radix_upsweep<<<ntiles, RS_T, 0, s>>>(kin, n, 8 * ps, hist, ntiles);
-    int e = fmm_device_scan_i32(hist, hist, nhist, sscr, fmm_scan_scratch_bytes(nhist), s, &t->launches);
+    k_radix_upsweep<<<ntiles, RS_T, 0, s>>>(kin, n, shift, db, hist, ntiles);
+    int e = fmm_device_scan_i32(hist, hist, nh, sscr, fmm_scan_scratch_bytes(nh), s, &t->launches);
     if (e) return e;
-    k_radix_downsweep<<<ntiles, RS_T, 0, s>>>(kin, vin, n, 8 * ps, hist, ntiles, kout, vout);
+    k_radix_downsweep<<<ntiles, RS_T, 0, s>>>(kin, vin, n, shift, db, hist, ntiles, kout, vout);
     t->launches += 2;
     FMM_CUDA_TRY(cudaGetLastError());
     kin = kout;
     vin = vout;
+    shift += db;
   }
   return FMM_OK;
 }
