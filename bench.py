@@ -58,11 +58,11 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 F_PAIR = 52.0
 # FP64 flops k_p2p_pairs executes per interaction (ncu, sm__sass_thread_inst_executed_op_
 # {dfma,dadd,dmul}_pred_on; profiles/r01/fp64_counts.json), for the executed-rate line
-F_EXEC = {"C4q": 31.47, "C4s": 29.48, "C4t": 31.21}
+F_EXEC = {"C4q": 31.17, "C4s": 29.02, "C4t": 30.92}
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu --set full,
-# profiles/r01/ncu_p2p_<cfg>_v10.txt); C4 = mean over its three launches.  The writes are the
+# profiles/r01/ncu_p2p_<cfg>_v16.txt); C4 = mean over its three launches.  The writes are the
 # per-(target, near slot) partial sums (m x nslot x 16 B) that k_p2p_finish adds.
-P2P_DRAM_BYTES_PER_LAUNCH = {"C4q": 2.887e9, "C4s": 2.809e9, "C4t": 4.074e9, "C4": 3.257e9}
+P2P_DRAM_BYTES_PER_LAUNCH = {"C4q": 2.847e9, "C4s": 2.411e9, "C4t": 3.995e9, "C4": 3.084e9}
 
 
 def log(*a):
