@@ -4,13 +4,15 @@
 //
 // Work unit = one (target leaf t, near leaf s) block.  In self mode (targets = sources,
 // reading D16) the near relation is symmetric, and so is the kernel up to the branch of
-// Arg: Log(x_i - x_j) = Log(x_j - x_i) +/- i pi, with the same log|z|^2.  A light
-// off-diagonal block (t < s) is therefore evaluated ONCE: every pair feeds the row
-// target (u_j Log(x_i - x_j)) and, reversed, the column target (u_i Log(x_j - x_i)).
-// Diagonal blocks, heavy blocks (split by rows) and the distinct-target configs use
-// one-sided blocks.  Every (target, near-leaf) pair of the near list owns one partial-sum
-// slot written by exactly one task in a fixed order, and a final pass adds the slots in
-// near-list order, so the result is deterministic.
+// Arg: Log(x_i - x_j) = Log(x_j - x_i) +/- i pi, with the same log|z|^2.  An off-diagonal
+// block (t < s) is therefore evaluated ONCE: every pair feeds the row target
+// (u_j Log(x_i - x_j)) and, reversed, the column target (u_i Log(x_j - x_i)).  Light blocks
+// (n_t n_s <= 65,536) are one task; heavy ones are split by rows of the larger leaf.  Light
+// diagonal blocks are symmetric as well (schedule below); heavy diagonal blocks and the
+// distinct-target configs are one-sided.  Every (target, near-leaf) pair of the near list
+// owns one partial-sum slot, and a final pass adds the slots in near-list order.  Each slot
+// is written by exactly one task, so the result is bitwise reproducible, except the column
+// slots of heavy symmetric blocks, which several row-range tasks add into atomically.
 #include <type_traits>
 
 #include "fmm_internal.cuh"
@@ -20,7 +22,7 @@ namespace {
 
 constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) block
 constexpr int P2P_S = 192;          // sources of one near leaf kept in shared memory per warp
-constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17;
+constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17, TF_HEAVY = 1 << 18;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -74,12 +76,29 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
         if (out) out[c] = make_int4(t, q | (qr << 8) | TF_SYM, 0, nt);
         ++c;
       }
-    } else {
-      if (t_in) emit_rows(t, q, nt, ns, 0);
-      if (s_in) emit_rows(s, qr, ns, nt, 0);
+    } else if (t_in || s_in) {
+      // heavy block: symmetric too, split by rows of the larger leaf; the smaller one is the
+      // column side (kept in shared memory when it fits) whose reactions from the row ranges
+      // are added atomically (their order is not fixed: reading D15's tolerance, not bits)
+      const bool t_rows = nt >= ns;
+      emit_rows(t_rows ? t : s, t_rows ? (q | (qr << 8)) : (qr | (q << 8)), t_rows ? nt : ns, t_rows ? ns : nt,
+                TF_SYM | TF_HEAVY);
     }
   }
   return c;
+}
+
+// zero the column-side slots of every heavy symmetric block (once per block: its r0 = 0 task)
+__global__ void k_heavy_zero(const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p,
+                             const int32_t* __restrict__ soff, const int32_t* __restrict__ near,
+                             double2* __restrict__ part, int nslot) {
+  const int ntask = *ntask_p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntask; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 tk = tasks[i];
+    if (!(tk.y & TF_HEAVY) || tk.z != 0) continue;
+    const int s = near[(int64_t)tk.x * FMM_NEAR_MAX + (tk.y & 0xff)], qr = (tk.y >> 8) & 0xff;
+    for (int j = soff[s]; j < soff[s + 1]; ++j) part[(int64_t)j * nslot + qr] = make_double2(0.0, 0.0);
+  }
 }
 
 __global__ void k_task_count(int64_t K, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     if (task >= ntask) break;
     const int4 tk = tasks[task];
     const int t = tk.x, q = tk.y & 0xff, qr = (tk.y >> 8) & 0xff;
-    const bool sym = tk.y & TF_SYM, diag = tk.y & TF_DIAG;
+    const bool sym = tk.y & TF_SYM, diag = tk.y & TF_DIAG, heavy = tk.y & TF_HEAVY;
     // symmetric diagonal block: a row step of rows [rc, rc + 8) and a 16-column half at a
     // skips the half when a + 15 < rc (those pairs arrive as reactions of earlier row steps),
     // evaluates it one-sided when it straddles the rows (a <= rc + 7; the pair (i, i) is the
@@ -319,7 +338,10 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
             s_re[cb + lane] = make_double2(o.x + Rr, o.y + Ri);
           } else if (write_react && lane < cnt) {
             double2* slot = part + ((int64_t)(sb + c0 + lane) * nslot + qr);
-            if (rc == tk.z) {
+            if (heavy) {
+              atomicAdd(&slot->x, Rr);
+              atomicAdd(&slot->y, Ri);
+            } else if (rc == tk.z) {
               *slot = make_double2(Rr, Ri);
             } else {
               const double2 o = *slot;
@@ -354,8 +376,17 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
       __syncwarp();
     }
     __syncwarp();
-    if (whole && write_react)
-      for (int i = lane; i < ns; i += 32) part[(int64_t)(sb + i) * nslot + qr] = s_re[i];
+    if (whole && write_react) {
+      if (heavy) {
+        for (int i = lane; i < ns; i += 32) {
+          double2* slot = part + (int64_t)(sb + i) * nslot + qr;
+          atomicAdd(&slot->x, s_re[i].x);
+          atomicAdd(&slot->y, s_re[i].y);
+        }
+      } else {
+        for (int i = lane; i < ns; i += 32) part[(int64_t)(sb + i) * nslot + qr] = s_re[i];
+      }
+    }
     __syncwarp();  // the next task restages s_xy / s_u / s_re
   }
 }
@@ -439,6 +470,11 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   const Geo& G = t->g;
   cudaStream_t s = t->stream;
   FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
+  if (G.self_mode) {
+    k_heavy_zero<<<148 * 4, 256, 0, s>>>(t->tasks, t->ntask, t->soff, t->near,
+                                                                        t->part, G.nslot);
+    t->launches++;
+  }
   FMM_CUDA_TRY(cudaFuncSetAttribute(k_p2p_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_SMEM));
   k_p2p_pairs<<<148 * P2P_MINB, 32 * P2P_WARPS, P2P_SMEM, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
                                        t->near, t->tperm, t->p2p_tab, t->part, G.nslot, t->leaf_lo, t->leaf_hi, t->status);

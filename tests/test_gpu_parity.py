@@ -190,3 +190,19 @@ def test_set_strengths_linearity():
     g.set_strengths(torch.from_numpy(2.0 * d["u"]).cuda())
     b = g.evaluate().cpu().numpy()
     assert normwise(b, 2 * a) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [9000, 24000])
+def test_heavy_blocks(n):
+    """Dense leaves: quadtree depth 2 (16 leaves) with n self points, so that near blocks
+    exceed 65,536 pairs (symmetric heavy tasks split by rows, reactions added atomically;
+    24000 points also puts leaves above the 192-point shared-memory limit) - against the
+    oracle within the D15 gate, and the self-pair exclusion holds in split diagonal blocks."""
+    w = SMALL_CASES["C4qs"].scaled(n, name=f"heavy{n}")
+    d = data(w)
+    g = gpu_tree(w, d, depth=2)
+    o = oracle_tree(w, d, depth=2)
+    phi = g.evaluate().cpu().numpy()
+    g.check()
+    ref = o.evaluate()
+    assert normwise(phi, ref) <= TOL
