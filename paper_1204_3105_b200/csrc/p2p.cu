@@ -180,6 +180,9 @@ __device__ __noinline__ PairOut p2p_slow(double dx, double dy, double r2, bool s
   return o;
 }
 
+// SELF: self mode (symmetric tasks possible); the distinct-target instantiation has no
+// reversed-pair work at all
+template <bool SELF>
 __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     if (task >= ntask) break;
     const int4 tk = tasks[task];
     const int t = tk.x, q = tk.y & 0xff, qr = (tk.y >> 8) & 0xff;
-    const bool sym = tk.y & TF_SYM, diag = tk.y & TF_DIAG, heavy = tk.y & TF_HEAVY;
+    const bool sym = SELF && (tk.y & TF_SYM), diag = SELF && (tk.y & TF_DIAG), heavy = SELF && (tk.y & TF_HEAVY);
     // symmetric diagonal block: a row step of rows [rc, rc + 8) and a 16-column half at a
     // skips the half when a + 15 < rc (those pairs arrive as reactions of earlier row steps),
     // evaluates it one-sided when it straddles the rows (a <= rc + 7; the pair (i, i) is the
@@ -475,9 +478,15 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
                                                                         t->part, G.nslot);
     t->launches++;
   }
-  FMM_CUDA_TRY(cudaFuncSetAttribute(k_p2p_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_SMEM));
-  k_p2p_pairs<<<148 * P2P_MINB, 32 * P2P_WARPS, P2P_SMEM, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy, t->sxy, t->su,
-                                       t->near, t->tperm, t->p2p_tab, t->part, G.nslot, t->leaf_lo, t->leaf_hi, t->status);
+  auto launch = [&](auto kern) -> int {
+    FMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_SMEM));
+    kern<<<148 * P2P_MINB, 32 * P2P_WARPS, P2P_SMEM, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy,
+                                                           t->sxy, t->su, t->near, t->tperm, t->p2p_tab, t->part,
+                                                           G.nslot, t->leaf_lo, t->leaf_hi, t->status);
+    return FMM_OK;
+  };
+  int e = G.self_mode ? launch(k_p2p_pairs<true>) : launch(k_p2p_pairs<false>);
+  if (e) return e;
   if (t->timing) cudaEventRecord(t->ev[7], s);
   const int64_t nl = t->leaf_hi - t->leaf_lo;
   if (nl > 0)
