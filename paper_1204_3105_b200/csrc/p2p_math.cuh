@@ -9,7 +9,7 @@
 //            (1/c_i, log c_i) selected by the top mantissa bits; |r| < 2^-8;
 //            log1p(r) by its Taylor series to r^7 (truncation < 2^-67).
 //   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/32 with k = round(32 t)
-//            from an FP32 estimate; atan t = atan t_k + atan q,
+//            from a MUFU.RCP64H estimate; atan t = atan t_k + atan q,
 //            q = (num - t_k den) / (den + t_k num), |q| <= 1/64 + 2^-20;
 //            atan q = q - q^3/3 + q^5/5 - q^7/7 + q^9/9 (truncation < 2^-66 |q|);
 //            the octant's offset and sign are folded into a table T[oct][k].
@@ -54,12 +54,6 @@ __device__ __forceinline__ double p2p_rcp(double b) {
   double e = fma(-b, r0, 1.0);
   e = fma(e, e, e);
   return fma(e, r0, r0);
-}
-
-__device__ __forceinline__ float p2p_rcpf(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
 }
 
 // 16-byte load from a 32-bit shared-space address
@@ -110,15 +104,14 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
 // so y - x never yields -0 there).
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
-  // FP32 estimate of t = min/max of |dx|, |dy| (|z| >= 1e-30 keeps the larger one a normal
-  // binary32; a smaller one that flushes to 0 only means t ~ 0)
-  float fx = fabsf(__double2float_rn(dx)), fy = fabsf(__double2float_rn(dy));
-  bool swap = fy > fx;
-  float tf = fminf(fx, fy) * p2p_rcpf(fmaxf(fx, fy));
-  int k = __float_as_int(fmaf(tf, 32.0f, 12582912.0f)) & 0x3f;  // round(32 t), 0..32
-  double num = swap ? dx : dy, den = swap ? dy : dx;
-  num = fabs(num);
-  den = fabs(den);
+  // t = min/max of |dx|, |dy| estimated with the MUFU reciprocal of the larger one (~2^-22)
+  // and rounded to k = round(32 t) by the 1.5 2^52 shift (FP64 pipe, no conversions)
+  const double ax = fabs(dx), ay = fabs(dy);
+  const bool swap = ay > ax;
+  const double num = swap ? ax : ay, den = swap ? ay : ax;
+  double r0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(den));
+  const int k = __double2loint(fma(num * r0, 32.0, 6755399441055744.0)) & 0x3f;  // round(32 t), 0..32
   // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
   const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
