@@ -57,6 +57,8 @@ extern "C" {
  *   FMM_TRIQUAD : root_x, root_y = centroid of the upright root triangle; root_size = its
  *                 circumradius R0 (level-l circumradius R0 * 2^-l).
  * depth  L: quadtree / triangle 1..15, septree 1..10 (leaf keys must fit 32 bits).
+ *           |root_x| + 2 root_size and |root_y| + 2 root_size must be < 1e20 (the P2P kernel
+ *           pads with points at 1e30), root_size > 0, all finite; else FMM_EBADCFG.
  * p       : expansion terms, 1..31 (multipole Q, a_1..a_p; local b_0..b_p).
  * self_mode: 1 when targets are the sources; the pair (i, i) is skipped by index (D16).
  * rank / nranks: target-leaf partition for multi-GPU runs;
@@ -98,10 +100,13 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
                    const double* tgt_xy, int64_t m, void* stream, fmm_tree_t* out);
 
 /* Evaluate Phi for all m targets of this rank: P2M, M2M (upward), M2L + L2L per
- * level (downward), then L2P fused with the P2P near field.  phi_out: m complex128
+ * level (downward), then the P2P near field and L2P.  phi_out: m complex128
  * values (interleaved re, im) in the caller's target order; device or host memory
  * (host: copied back on `stream`; the caller synchronises the stream).  Targets
- * owned by other ranks are left untouched. */
+ * owned by other ranks are left untouched.  Repeated evaluations are bitwise
+ * identical unless the tree has heavy symmetric near blocks (self mode, two leaves
+ * with n_t n_s > 65,536 points pairs), whose column sums are added atomically (equal
+ * to rounding). */
 int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream);
 
 /* Replace the strengths (same geometry) so the tree can be re-evaluated. */
