@@ -33,7 +33,7 @@ def main():
         ms = (time.perf_counter() - t0) * 1e3
         st = t.stage_times()
         c = t.export(X.COUNTERS)
-        print(f"{name} rep {r}: {ms:.2f} ms wall (build {tb:.2f}), upward {st[3]:.3f} down {st[4]:.3f} p2p {st[5]:.3f} ms; "
+        print(f"{name} rep {r}: {ms:.2f} ms wall (build {tb:.2f}), upward {st[3]:.3f} down {st[4]:.3f} p2p {st[5]:.3f} (pairs kernel {st[2]:.3f}) ms; "
               f"pairs {c[1]} m2l {c[0]} launches {t.launch_count()}", flush=True)
         t.check()
         t.close()
