@@ -353,11 +353,17 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   __syncwarp();
   for (int b0 = 0; b0 < nsrc; b0 += NB) {
     const int nb = min(NB, nsrc - b0);
-    // powers: lane = (source s = lane / 4, residue j = lane % 4): w^(4m + j), m = 0..P/4
+    // lane = (source s = lane / 4, residue j = lane % 4) owns exponents k = 4m + j: it loads
+    // a_{s,k} (all its loads first), forms w^k and a~_{s,k} = (-1)^k a_{s,k} w^k directly
     {
+      constexpr int NM = P / 4 + 1;
       const int s = lane >> 2, j = lane & 3;
       if (s < nb) {
         const int src = s_src[b0 + s];
+        const double2* ab = mp_l + (int64_t)src * (p + 1);
+        double2 av[NM];
+#pragma unroll
+        for (int m = 0; m < NM; ++m) av[m] = (4 * m + j <= p) ? ab[4 * m + j] : make_double2(0.0, 0.0);
         const double2 cs = cen_l[src];
         const double zx = cs.x - ct.x, zy = cs.y - ct.y;
         const double d = p2p_rcp(fma(zx, zx, zy * zy));
@@ -366,34 +372,21 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
         const double2 w4 = cmul(w2, w2);
         double2 pw = j == 0 ? make_double2(1.0, 0.0) : (j == 1 ? wv : (j == 2 ? w2 : cmul(w2, wv)));
 #pragma unroll
-        for (int m = 0; 4 * m + j <= P && m <= P / 4; ++m) {
-          if (4 * m + j <= P) s_pw[s * (P + 1) + 4 * m + j] = pw;
+        for (int m = 0; m < NM; ++m) {
+          const int k = 4 * m + j;
+          if (k <= P) s_pw[s * (P + 1) + k] = pw;
+          if (k >= 1 && k <= P) {
+            double2 v = cmul(av[m], pw);
+            if (k & 1) v = make_double2(-v.x, -v.y);
+            s_at[s * P + k - 1] = v;
+          }
           pw = cmul(pw, w4);
         }
         if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
           const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
           s_lg[s] = make_double2(0.5 * p2p_log(fma(dx, dx, dy * dy), a_log), p2p_atan2(dy, dx, a_atan));
-          s_q[s] = mp_l[(int64_t)src * (p + 1)].x;
+          s_q[s] = av[0].x;
         }
-      }
-    }
-    __syncwarp();
-    // a~_{s,k} = (-1)^k a_{s,k} w_s^k: all loads of the batch first, then the products
-    static_assert((NB * P) % 32 == 0, "a~ staging assumes whole warp rounds");
-    constexpr int NR = NB * P / 32;
-    {
-      double2 av[NR];
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        const int idx = lane + 32 * i, s = idx / P, k = idx % P + 1;
-        av[i] = (s < nb && k <= p) ? mp_l[(int64_t)s_src[b0 + s] * (p + 1) + k] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        const int idx = lane + 32 * i, s = idx / P, k = idx % P + 1;
-        double2 v = cmul(av[i], s_pw[s * (P + 1) + k]);
-        if (k & 1) v = make_double2(-v.x, -v.y);
-        s_at[idx] = v;  // = s_at[s * P + k - 1]
       }
     }
     __syncwarp();
