@@ -158,16 +158,17 @@ def run_gpu(args):
         host_in[nm] = tuple(None if a is None else torch.from_numpy(a).pin_memory()
                             for a in (d["src_xy"], d["u"], d["tgt_xy"]))
         outs[nm] = torch.zeros(w.m, dtype=torch.complex128, device=dev)
-        host_out[nm] = torch.zeros(w.m, dtype=torch.complex128).pin_memory()
+        host_out[nm] = [torch.zeros(w.m, dtype=torch.complex128).pin_memory() for _ in range(2)]
 
-    # e2e: one CUDA stream per tiling, so that the host<->device copies of one problem overlap
-    # the kernels of the others (the step joins them on the timing stream).  The device-resident
-    # timed region keeps one stream, so that each kernel's event time is its own (roofline).
-    side = {nm: torch.cuda.Stream(dev) for nm in names}
+    # e2e: two CUDA streams per tiling, alternating by step (double buffering), so that the
+    # host<->device copies of one step overlap the kernels of the previous step and of the other
+    # tilings; all streams join before the end event.  The device-resident timed region keeps
+    # one stream, so that each kernel's event time is its own (roofline).
+    side = [{nm: torch.cuda.Stream(dev) for nm in names} for _ in range(2)]
 
-    def one_step(timing=False, host=False, fork=True, join=True):
+    def one_step(timing=False, host=False, fork=True, join=True, parity=0):
         launches, stage = 0, {}
-        streams = side if (host and not args.serial) else {nm: stream for nm in names}
+        streams = side[parity] if (host and not args.serial) else {nm: stream for nm in names}
         for nm in names:
             if fork and streams[nm] is not stream:
                 streams[nm].wait_stream(stream)
@@ -175,7 +176,7 @@ def run_gpu(args):
             src, u, tgt = host_in[nm] if host else dev_in[nm]
             st = streams[nm]
             t = fmm.Tree(cfg_of(w, timing), src, u, tgt, stream=st)
-            t.evaluate(host_out[nm] if host else outs[nm], stream=st)
+            t.evaluate(host_out[nm][parity] if host else outs[nm], stream=st)
             launches += t.launch_count()
             if timing:
                 stage[nm] = t
@@ -264,7 +265,7 @@ def run_gpu(args):
     # consecutive steps pipeline: a tiling's next H2D copy waits only for its own previous
     # step (its stream), not for the other tilings; all streams join before the end event
     for s in range(args.steps):
-        one_step(host=True, fork=(s == 0), join=(s == args.steps - 1))
+        one_step(host=True, fork=(s < 2), join=(s >= args.steps - 2), parity=s % 2)
     f1.record(stream)
     barrier()
     e2e_ms = f0.elapsed_time(f1)
@@ -319,7 +320,7 @@ def run_gpu(args):
         "data": "synthetic, seeded numpy PCG64 (fmm_inputs), shapes of BASELINE.json configs",
         "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
                    "tilings": names, "step": "fmm_build_tree + fmm_evaluate per tiling",
-                   "streams": "timed region: one stream; e2e: " + ("one stream" if args.serial else "one CUDA stream per tiling (copies overlap other tilings' kernels, steps pipelined), joined at the end"),
+                   "streams": "timed region: one stream; e2e: " + ("one stream" if args.serial else "two CUDA streams per tiling alternating by step (copies overlap kernels), joined at the end"),
                    "l2": "inputs larger than L2 (>= 400 MB per tiling)", "per_tiling": per_tiling},
         "roofline": roof,
         "roofline_m2l": roof_m2l,
