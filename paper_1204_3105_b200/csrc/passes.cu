@@ -445,11 +445,8 @@ static void launch_down(fmm_tree_s* t, int l) {
   const int64_t nc = G.ncells[l];
   static const bool simt = getenv("FMM_M2L_SIMT") && getenv("FMM_M2L_SIMT")[0] == '1';
   if (!simt) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_down_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DownSmem<P>::bytes);
-      attr = true;
-    }
+    // per device (a process may drive several GPUs); a failure surfaces as the launch error
+    cudaFuncSetAttribute(k_down_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DownSmem<P>::bytes);
     k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, DownSmem<P>::bytes, t->stream>>>(
         l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
