@@ -57,17 +57,22 @@ void fmm_host_p2p_tables(double* tab) {
 
 namespace {
 
+// keep freed tree memory in each device's stream-ordered pool (release threshold = max), once
+// per device: trees are built and freed every step, and returning memory to the driver in
+// between would make every build pay for fresh allocations
 void init_pool_once() {
-  static std::once_flag f;
-  std::call_once(f, [] {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev]) return;
+  done[dev] = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
 }
 
 bool is_device_ptr(const void* p) {
