@@ -34,7 +34,7 @@ std::vector<double> host_binom() {
 void fmm_host_p2p_tables(double* tab) {
   for (int i = 0; i < P2P_LOG_N; ++i) {
     // interval centre: the value of the centre bit pattern (exactly 1.0 for the interval of 1.0)
-    uint64_t mid = P2P_LOG_OFF + ((uint64_t)i << 45) + ((uint64_t)1 << 44);
+    uint64_t mid = P2P_LOG_OFF + ((uint64_t)i << P2P_LOG_SHIFT) + ((uint64_t)1 << (P2P_LOG_SHIFT - 1));
     double c;
     memcpy(&c, &mid, 8);
     double invc = 1.0 / c;

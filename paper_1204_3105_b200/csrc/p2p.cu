@@ -139,7 +139,7 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 constexpr int P2P_RS = 32;  // row stride (double2) of the reaction scratch; column c of row lane r sits at c ^ 2r
                             // (conflict-free STS.128 / LDS.128)
 // dynamic shared memory of one block: tables, then per warp sources, strengths, reactions, scratch
-constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1) + 32);
+constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1) + 64);
 constexpr size_t P2P_WARP_BYTES = sizeof(double2) * (2 * P2P_S + 4 * P2P_RS) + sizeof(double) * P2P_S;
 constexpr size_t P2P_SMEM = P2P_TAB_BYTES + P2P_WARPS * P2P_WARP_BYTES;
 constexpr double P2P_PAD = 1.0e30;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     int64_t lo, int64_t hi, DevStatus* st) {
   extern __shared__ double2 smem[];
   double2* s_log = smem;
-  double2* s_atan = s_log + P2P_LOG_N;  // + 32 pad: garbage indices of |z| < 1e-30
+  double2* s_atan = s_log + P2P_LOG_N;  // + 64 pad: garbage indices of |z| < 1e-30
   p2p_load_tables(tabs, s_log, s_atan);
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

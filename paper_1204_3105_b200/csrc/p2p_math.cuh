@@ -5,33 +5,34 @@
 // pair loop ~4x slower.  Valid for |z| >= 1e-30 (the caller sends
 // smaller |z|, including the excluded / coincident z = 0, to an exact slow path).
 //
-//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 128-entry table of
-//            (1/c_i, log c_i) selected by the top mantissa bits; |r| < 2^-8;
-//            log1p(r) by its Taylor series to r^7 (truncation < 2^-67).
-//   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/32 with k = round(32 t)
+//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 256-entry table of
+//            (1/c_i, log c_i) selected by the top mantissa bits; |r| < 2^-8.4;
+//            log1p(r) by its Taylor series to r^6 (truncation < 2^-61 |r|).
+//   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/64 with k = round(64 t)
 //            from a MUFU.RCP64H estimate; atan t = atan t_k + atan q,
-//            q = (num - t_k den) / (den + t_k num), |q| <= 1/64 + 2^-20;
-//            atan q = q - q^3/3 + q^5/5 - q^7/7 + q^9/9 (truncation < 2^-66 |q|);
+//            q = (num - t_k den) / (den + t_k num), |q| <= 1/128 + 2^-20;
+//            atan q = q - q^3/3 + q^5/5 - q^7/7 (truncation < 2^-62 |q|);
 //            the octant's offset and sign are folded into a table T[oct][k].
 //   division: MUFU.RCP64H estimate + one cubic Newton step (e + e^2), error ~ e^3.
 // Polynomial coefficients live in the constant bank (DFMA operands, no register moves).
 #pragma once
 #include <stdint.h>
 
-#define P2P_LOG_N 128
+#define P2P_LOG_N 256
 #define P2P_TW 8  // targets per P2P warp task
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
-#define P2P_ATAN_K 32  // t_k = k / 32, k = 0..32
-// table layout (doubles): [0, 256) log (1/c, log c) pairs; [256, 256 + 2*8*33) (T[oct][k], t_k)
+#define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
+// table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (T[oct][k], t_k), 8 x (K+1)
 #define P2P_TAB_LOG 0
-#define P2P_TAB_ATAN 256
-#define P2P_TAB_DOUBLES (256 + 2 * 8 * (P2P_ATAN_K + 1))
+#define P2P_TAB_ATAN (2 * P2P_LOG_N)
+#define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * 8 * (P2P_ATAN_K + 1))
 // |z|^2 below this (hi word of 1e-60) takes the exact slow path
 #define P2P_SLOW_HI 0x3379b604
-// z intervals: bit patterns [OFF + i 2^45, OFF + (i+1) 2^45), OFF = 0x3fe6000000000000 - 2^44,
-// so that the bit pattern of 1.0 is the centre of interval 80
-#define P2P_LOG_OFF_HI 0x3fe5f000
-#define P2P_LOG_OFF 0x3fe5f00000000000ull
+// z intervals: bit patterns [OFF + i 2^44, OFF + (i+1) 2^44), OFF = 0x3fe6000000000000 - 2^43,
+// so that the bit pattern of 1.0 is the centre of interval 160
+#define P2P_LOG_OFF_HI 0x3fe5f800
+#define P2P_LOG_OFF 0x3fe5f80000000000ull
+#define P2P_LOG_SHIFT 44
 
 __constant__ double P2P_C[13] = {
     1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,  // log1p Taylor r^7 .. r^2
@@ -72,21 +73,20 @@ __device__ __forceinline__ uint32_t p2p_smem_addr(const void* p) {
 }
 
 // log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
-// The 128 intervals of z are centred so that z = 1 is the centre of its interval
+// The 256 intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
 __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
   int hi = __double2hiint(r2), lo = __double2loint(r2);
   int tmp = hi - P2P_LOG_OFF_HI;
-  int i = (tmp >> 13) & (P2P_LOG_N - 1);
+  int i = (tmp >> (P2P_LOG_SHIFT - 32)) & (P2P_LOG_N - 1);
   int k = tmp >> 20;  // arithmetic shift
   double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
   const double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
-  // r^5..r^7 coefficients rounded to 20-bit mantissas (SASS immediates): their error
-  // (< 2^-21 relative) times r^n/n stays below 2^-60 for |r| <= 2^-8
-  double q = fma(r, 0x1.2492400000000p-3 /* ~1/7 */, -0x1.5555500000000p-3 /* ~-1/6 */);
-  q = fma(q, r, 0x1.9999900000000p-3 /* ~1/5 */);
+  // r^5, r^6 coefficients rounded to 20-bit mantissas (SASS immediates): their error
+  // (< 2^-21 relative) times r^n/n stays below 2^-62 for |r| <= 2^-8.4
+  double q = fma(r, -0x1.5555500000000p-3 /* ~-1/6 */, 0x1.9999900000000p-3 /* ~1/5 */);
   q = fma(q, r, -0.25);
   q = fma(q, r, P2P_C[4]);  // 1/3 (full precision)
   q = fma(q, r, -0.5);
@@ -105,13 +105,13 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // so y - x never yields -0 there).
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
   // t = min/max of |dx|, |dy| estimated with the MUFU reciprocal of the larger one (~2^-22)
-  // and rounded to k = round(32 t) by the 1.5 2^52 shift (FP64 pipe, no conversions)
+  // and rounded to k = round(64 t) by the 1.5 2^52 shift (FP64 pipe, no conversions)
   const double ax = fabs(dx), ay = fabs(dy);
   const bool swap = ay > ax;
   const double num = swap ? ax : ay, den = swap ? ay : ax;
   double r0;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(den));
-  const int k = __double2loint(fma(num * r0, 32.0, 6755399441055744.0)) & 0x3f;  // round(32 t), 0..32
+  const int k = __double2loint(fma(num * r0, (double)P2P_ATAN_K, 6755399441055744.0)) & 0x7f;  // 0..64
   // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
   const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
@@ -120,9 +120,8 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   double b = fma(Tt.y, num, den);
   double q = a * p2p_rcp(b);
   double q2 = q * q;
-  // q^7, q^9 coefficients rounded to 20-bit mantissas (immediates), error < 2^-60 |q|
-  double P = fma(q2, 0x1.c71c700000000p-4 /* ~1/9 */, -0x1.2492400000000p-3 /* ~-1/7 */);
-  P = fma(P, q2, P2P_C[8]);  // 1/5
+  // q^7 coefficient rounded to a 20-bit mantissa (immediate), error < 2^-62 |q|
+  double P = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
   P = fma(P, q2, P2P_C[9]);  // -1/3
   double at = fma(q * q2, P, q);
   // sign S = (-1)^(swap + dxneg + dyneg) applied by flipping the sign bit
