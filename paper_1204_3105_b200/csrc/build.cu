@@ -131,6 +131,18 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_apply(const int32_t* in, int64_
 // counters, so each tile needs only two block barriers per pass.
 constexpr int RS_W = 8, RS_T = 32 * RS_W, RS_SEG = 512, RS_TILE = RS_W * RS_SEG, RS_MAXB = 10;
 
+// lanes of the warp holding the same db-bit digit as this lane (valid lanes only): one ballot
+// per digit bit (cheaper than match.any, whose latency bounded the sort)
+__device__ __forceinline__ unsigned radix_peers(unsigned d, int db, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+  for (int b = 0; b < db; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
 __global__ void __launch_bounds__(RS_T) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                           int db, int32_t* __restrict__ tile_hist, int ntiles) {
   __shared__ int cnt[RS_W][1 << RS_MAXB];
@@ -142,8 +154,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_upsweep(const uint32_t* __restri
   for (int r = 0; r < RS_SEG / 32; ++r) {
     const int64_t i = seg0 + 32 * r + lane;
     const bool valid = i < n;
-    const unsigned d = valid ? ((keys[i] >> shift) & mask) : (unsigned)(nb + lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned d = valid ? ((keys[i] >> shift) & mask) : 0u;
+    const unsigned peers = radix_peers(d, db, valid);
     if (valid && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
     __syncwarp();
   }
@@ -171,8 +183,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __rest
   for (int r = 0; r < RS_SEG / 32; ++r) {
     const int64_t i = seg0 + 32 * r + lane;
     const bool valid = i < n;
-    const unsigned d = valid ? ((keys[i] >> shift) & mask) : (unsigned)(nb + lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned d = valid ? ((keys[i] >> shift) & mask) : 0u;
+    const unsigned peers = radix_peers(d, db, valid);
     if (valid && lane == __ffs(peers) - 1) wb[w][d] += __popc(peers);
     __syncwarp();
   }
@@ -193,8 +205,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __rest
     const int64_t i = seg0 + 32 * r + lane;
     const bool valid = i < n;
     const uint32_t k = valid ? keys[i] : 0u;
-    const unsigned d = valid ? ((k >> shift) & mask) : (unsigned)(nb + lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned d = valid ? ((k >> shift) & mask) : 0u;
+    const unsigned peers = radix_peers(d, db, valid);
     int pos = 0;
     if (valid) pos = wb[w][d] + __popc(peers & lt);
     __syncwarp();
