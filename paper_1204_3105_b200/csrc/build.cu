@@ -311,13 +311,16 @@ __global__ void k_e4mask_level(DGeo g, int l, const int32_t* __restrict__ toff, 
     const int64_t P = t / g.B;
     const int nc = ncand[P];
     const int32_t* c = cand + P * FMM_CAND_MAX;
-    int64_t nb[16];
+    int64_t nb[17];
     int nn = geo_neighbors(g, l, t, nb);
+    nb[nn++] = t;
+    sort_small(nb, nn);
+    // both lists ascending: one merge pass marks the candidates outside {t} U Neighbors(t)
+    int k = 0;
     for (int i = 0; i < nc; ++i) {
       const int64_t ci = c[i];
-      bool near = (ci == t);
-      for (int k = 0; k < nn; ++k) near |= (ci == nb[k]);
-      if (!near) mask |= 1ull << i;
+      while (k < nn && nb[k] < ci) ++k;
+      if (!(k < nn && nb[k] == ci)) mask |= 1ull << i;
     }
   }
   e4mask[t] = mask;
