@@ -55,7 +55,7 @@ def main():
         for k, d in per.items():
             fl = flops(d)
             ms = d["gpu__time_duration.sum"] / 1e6
-            units = pairs if k == "k_p2p_pairs" else m2l
+            units = pairs if k.startswith("k_p2p_pairs") else m2l
             res[k] = {"fp64_flops": fl, "dmma_warp_inst": d.get("smsp__inst_executed_pipe_tensor_subpipe_dmma.sum", 0.0),
                       "launches": d["launches"], "kernel_ms_under_ncu": ms, "units": units,
                       "flops_per_unit": fl / units, "executed_tflops_under_ncu": fl / (ms / 1e3) / 1e12}
