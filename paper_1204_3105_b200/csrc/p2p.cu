@@ -7,12 +7,12 @@
 // Arg: Log(x_i - x_j) = Log(x_j - x_i) +/- i pi, with the same log|z|^2.  An off-diagonal
 // block (t < s) is therefore evaluated ONCE: every pair feeds the row target
 // (u_j Log(x_i - x_j)) and, reversed, the column target (u_i Log(x_j - x_i)).  Light blocks
-// (n_t n_s <= 65,536) are one task; heavy ones are split by rows of the larger leaf.  Light
-// diagonal blocks are symmetric as well (schedule below); heavy diagonal blocks and the
+// (n_t n_s <= 65,536) are one task; heavy ones are split by rows of the larger leaf.
+// Diagonal blocks are symmetric as well (schedule below; heavy ones split by rows); the
 // distinct-target configs are one-sided.  Every (target, near-leaf) pair of the near list
 // owns one partial-sum slot, and a final pass adds the slots in near-list order.  Each slot
-// is written by exactly one task, so the result is bitwise reproducible, except the column
-// slots of heavy symmetric blocks, which several row-range tasks add into atomically.
+// is written by exactly one task, so the result is bitwise reproducible, except the slots of
+// heavy symmetric blocks, which several row-range tasks add into atomically.
 #include <type_traits>
 
 #include "fmm_internal.cuh"
@@ -61,7 +61,9 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
           if (out) out[c] = make_int4(t, q | (q << 8) | TF_SYM | TF_DIAG, 0, nt);
           ++c;
         } else {
-          emit_rows(t, q, nt, ns, TF_DIAG);
+          // heavy diagonal: symmetric row ranges; rows and reactions meet in slot q and are
+          // added atomically (zeroed by k_heavy_zero)
+          emit_rows(t, q | (q << 8), nt, ns, TF_SYM | TF_DIAG | TF_HEAVY);
         }
       }
       continue;
@@ -368,11 +370,15 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
         for (int k = 0; k < 8; ++k) v += sd_[(k * 8 + rr) * 2 + comp];
         const int row = rc + (rr & 3) + 4 * (rr >> 2);
         if (row < tk.w) {
-          if (sd) {  // rows and reactions of a diagonal block share the slots: add into s_re
+          if (sd && whole) {  // rows and reactions of a diagonal block share the slots: add into s_re
             double* re_ = (double*)(s_re + row) + comp;
             *re_ += v;
           } else if (write_rows) {
-            ((double*)(part + (int64_t)(tb + row) * nslot + q))[comp] = v;
+            double* dst = (double*)(part + (int64_t)(tb + row) * nslot + q) + comp;
+            if (sd)  // heavy diagonal: slot shared with the reactions of other row ranges
+              atomicAdd(dst, v);
+            else
+              *dst = v;
           }
         }
       }
