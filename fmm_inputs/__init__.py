@@ -208,3 +208,58 @@ def generate(w: Workload):
 
 def get(name: str) -> Workload:
     return WORKLOADS[name]
+
+
+# ---------------------------------------------------------------- section-9 sweeps (NEXT-1)
+# "S_opt uniformly random source and target points fitted to each cell ... to modify the total
+# number of source and target points, the total number of occupied cells is reduced".
+# Leaf cells are enumerated geometrically (a sampling recipe; no CellIndex arithmetic here).
+def s_opt(tiling: str, p: int) -> float:
+    """Table 2 optimal points per cell at N = M: p (P2'/P4)^0.5."""
+    return p * {"quad": 116.0 / 27.0, "sept": 308.0 / 42.0, "triq": 164.0 / 39.0}[tiling] ** 0.5
+
+
+def leaf_cells(tiling: str, depth: int, root_x: float, root_y: float, root_size: float):
+    """-> (centres (K, 2), circumradius, nsides, angle0 (K,)) of every leaf polygon."""
+    if tiling == "quad":
+        n = 2 ** depth
+        s = root_size / n
+        i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        c = np.stack([root_x + (i.ravel() + 0.5) * s, root_y + (j.ravel() + 0.5) * s], axis=1)
+        return c, s / math.sqrt(2.0), 4, np.full(len(c), math.pi / 4.0)
+    if tiling == "sept":
+        c = island_leaf_centres(root_size, depth) + np.array([root_x, root_y])
+        return c, sept_leaf_r(root_size, depth), 6, np.zeros(len(c))
+    # triangle: midpoint subdivision of the upright root (centroid root_x, root_y, circumradius)
+    R = root_size
+    v = np.array([[root_x + R * math.cos(math.pi / 2 + 2 * math.pi * k / 3),
+                   root_y + R * math.sin(math.pi / 2 + 2 * math.pi * k / 3)] for k in range(3)])[None]
+    for _ in range(depth):
+        a, b, c3 = v[:, 0], v[:, 1], v[:, 2]
+        ab, bc, ca = 0.5 * (a + b), 0.5 * (b + c3), 0.5 * (c3 + a)
+        v = np.concatenate([np.stack(t, axis=1) for t in ((a, ab, ca), (ab, b, bc), (ca, bc, c3), (bc, ca, ab))])
+    cen = v.mean(axis=1)
+    up = v[:, 0, 1] > cen[:, 1]  # first vertex above the centroid: upright
+    return cen, R * 2.0 ** -depth, 3, np.where(up, math.pi / 2.0, -math.pi / 2.0)
+
+
+def sweep_generate(tiling: str, depth: int, root_x: float, root_y: float, root_size: float, per_cell: int,
+                   n_cells: int, seed: int):
+    """n_cells occupied leaves (a seeded random subset), per_cell uniform sources and as many
+    distinct uniform targets in each; strengths U[-1, 1).  -> dict like generate()."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cen, rad, ns, ang = leaf_cells(tiling, depth, root_x, root_y, root_size)
+    occ = rng.choice(len(cen), size=min(n_cells, len(cen)), replace=False)
+
+    def pts():
+        cell = np.repeat(occ, per_cell)
+        px, py = polygon_points(rng, len(cell), ns, rad, 0.0)
+        a = ang[cell]  # polygon_points puts a vertex at angle 0: rotate to the cell's orientation
+        ca, sa = np.cos(a), np.sin(a)
+        return np.stack([cen[cell, 0] + ca * px - sa * py, cen[cell, 1] + sa * px + ca * py], axis=1)
+
+    src = pts()
+    u = rng.uniform(-1.0, 1.0, len(src))
+    tgt = pts()
+    return {"src_xy": np.ascontiguousarray(src, np.float64), "u": np.ascontiguousarray(u, np.float64),
+            "tgt_xy": np.ascontiguousarray(tgt, np.float64)}

@@ -179,6 +179,16 @@ int64_t fmm_launch_count(fmm_tree_t t);
 
 void fmm_free(fmm_tree_t t);
 
+/* Direct evaluation (the reference of the paper's section-9 error and
+ * runtime sweeps): phi_out[j] = sum_i src_u[i] Log(tgt_j - src_i) over all n
+ * sources, O(n m), principal branch with a canonical +0 imaginary zero (D13); in self_mode
+ * (targets = sources, m == n, tgt_xy ignored) the pair i == j is skipped (D16).  Pointers as
+ * in fmm_build_tree (device used in place, host staged on `stream`); phi_out m complex128 on
+ * the device or host.  Synchronises `stream`.  Returns FMM_ECOINCIDENT (message names the
+ * smallest target index) when a target coincides with a source of another index. */
+int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const double* tgt_xy, int64_t m,
+               int32_t self_mode, double* phi_out, void* stream);
+
 /* Test hook: the P2P kernel's FP64 math on n explicit offsets z = dx + i dy (device
  * pointers, interleaved): out[2i] = log|z|^2, out[2i+1] = Arg z in (-pi, pi] with a zero
  * imaginary part read as +0 (D13).  z must have a normal |z|^2 (the kernel

@@ -15,6 +15,7 @@ from .native import (  # noqa: F401
     QUADTREE,
     SEPTREE,
     TRIQUAD,
+    direct,
 )
 
-__all__ = ["Config", "FmmError", "Tree", "X", "lib", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]
+__all__ = ["Config", "FmmError", "Tree", "X", "direct", "lib", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]

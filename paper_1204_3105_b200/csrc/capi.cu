@@ -492,6 +492,53 @@ int64_t fmm_launch_count(fmm_tree_t t) { return t ? t->launches : -1; }
 
 void fmm_free(fmm_tree_t t) { free_tree(t); }
 
+int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const double* tgt_xy, int64_t m,
+               int32_t self_mode, double* phi_out, void* stream) {
+  if (n < 0 || m < 0 || (self_mode && m != n)) return FMM_EBADCFG;
+  if (m == 0) return FMM_OK;
+  if (!phi_out || (n > 0 && (!src_xy || !src_u)) || (!self_mode && !tgt_xy)) return FMM_EBADCFG;
+  cudaStream_t s = (cudaStream_t)stream;
+  // device copies of host inputs / output, the P2P tables and the error word in one allocation
+  const bool dsx = is_device_ptr(src_xy), dsu = is_device_ptr(src_u), dphi = is_device_ptr(phi_out);
+  const double* t_in = self_mode ? src_xy : tgt_xy;
+  const bool dtx = is_device_ptr(t_in);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_sx = dsx ? 0 : take((size_t)n * 16), o_su = dsu ? 0 : take((size_t)n * 8);
+  const size_t o_tx = (dtx || self_mode) ? 0 : take((size_t)m * 16), o_phi = dphi ? 0 : take((size_t)m * 16);
+  const size_t o_tab = take(P2P_TAB_DOUBLES * 8), o_bad = take(8);
+  char* buf = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, off, s));
+  const double* sx = dsx ? src_xy : (const double*)(buf + o_sx);
+  const double* su = dsu ? src_u : (const double*)(buf + o_su);
+  if (!dsx) FMM_CUDA_TRY(cudaMemcpyAsync(buf + o_sx, src_xy, (size_t)n * 16, cudaMemcpyHostToDevice, s));
+  if (!dsu) FMM_CUDA_TRY(cudaMemcpyAsync(buf + o_su, src_u, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  const double* tx = self_mode ? sx : (dtx ? tgt_xy : (const double*)(buf + o_tx));
+  if (!self_mode && !dtx) FMM_CUDA_TRY(cudaMemcpyAsync(buf + o_tx, tgt_xy, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+  double* ph = dphi ? phi_out : (double*)(buf + o_phi);
+  std::vector<double> tab(P2P_TAB_DOUBLES);
+  fmm_host_p2p_tables(tab.data());
+  FMM_CUDA_TRY(cudaMemcpyAsync(buf + o_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
+  FMM_CUDA_TRY(cudaMemsetAsync(buf + o_bad, 0xff, 8, s));
+  int e = fmm_direct_launch(sx, su, n, tx, m, self_mode, (const double*)(buf + o_tab), ph,
+                            (unsigned long long*)(buf + o_bad), s);
+  unsigned long long bad = ~0ull;
+  if (!e && !dphi) FMM_CUDA_TRY(cudaMemcpyAsync(phi_out, ph, (size_t)m * 16, cudaMemcpyDeviceToHost, s));
+  if (!e) FMM_CUDA_TRY(cudaMemcpyAsync(&bad, buf + o_bad, 8, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(buf, s);
+  if (e) return e;
+  if (bad != ~0ull) {
+    fmm_set_error_message("coincident source and target at target index " + std::to_string(bad));
+    return FMM_ECOINCIDENT;
+  }
+  return FMM_OK;
+}
+
 int fmm_debug_p2p_math(const double* dxdy, int64_t n, double* out, void* stream) {
   if (n <= 0) return FMM_OK;
   if (!is_device_ptr(dxdy) || !is_device_ptr(out)) return FMM_EBADCFG;

@@ -118,3 +118,5 @@ int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);
 int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s);
 // capi.cu
 void fmm_host_p2p_tables(double* tab);  // fills P2P_TAB_DOUBLES doubles
+int fmm_direct_launch(const double* sxy, const double* su, int64_t n, const double* txy, int64_t m, int self_mode,
+                      const double* tabs, double* phi, unsigned long long* bad, cudaStream_t s);

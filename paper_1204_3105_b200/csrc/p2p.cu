@@ -441,6 +441,64 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
   }
 }
 
+// ------------------------------------------------------------------ direct sum (NEXT-1)
+// Phi_j = sum_i u_i Log(y_j - x_i) over ALL sources (self mode: i != j by index, D16), the
+// reference the paper's section-9 error sweeps compare against.  A lane owns one target; the
+// block stages 128 sources at a time in shared memory; the same pair math as the near field
+// (fast path, exact slow path for |z| < 1e-30).  Coincident pairs (other than i == j in self
+// mode) set *bad to the smallest target index involved.
+constexpr int DIR_T = 128;
+__global__ void __launch_bounds__(DIR_T) k_direct(const double2* __restrict__ sxy, const double* __restrict__ su,
+                                                  int64_t n, const double2* __restrict__ txy, int64_t m,
+                                                  int self_mode, const double* __restrict__ tabs,
+                                                  double2* __restrict__ phi, unsigned long long* bad) {
+  __shared__ double2 s_log[P2P_LOG_N];
+  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1) + 64];
+  __shared__ double2 s_x[DIR_T];
+  __shared__ double s_u[DIR_T];
+  p2p_load_tables(tabs, s_log, s_atan);
+  const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
+  const int64_t j = blockIdx.x * (int64_t)DIR_T + threadIdx.x;
+  const bool tv = j < m;
+  // canonical +0 imaginary zero of y - x (D13): coordinates read as x + 0
+  double2 y = tv ? txy[j] : make_double2(P2P_PAD, P2P_PAD);
+  y = make_double2(__dadd_rn(y.x, 0.0), __dadd_rn(y.y, 0.0));
+  double re = 0.0, im = 0.0;
+  for (int64_t c0 = 0; c0 < n; c0 += DIR_T) {
+    __syncthreads();
+    const int64_t i = c0 + threadIdx.x;
+    if (i < n) {
+      const double2 x = sxy[i];
+      s_x[threadIdx.x] = make_double2(__dadd_rn(x.x, 0.0), __dadd_rn(x.y, 0.0));
+      s_u[threadIdx.x] = su[i];
+    } else {
+      s_x[threadIdx.x] = make_double2(-P2P_PAD, P2P_PAD);
+      s_u[threadIdx.x] = 0.0;
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)DIR_T, n - c0);
+    for (int k = 0; k < cnt; ++k) {
+      const double2 x = s_x[k];
+      const double dx = y.x - x.x, dy = y.y - x.y;
+      const double r2 = fma(dx, dx, dy * dy);
+      PairOut pr = p2p_fast(dx, dy, r2, a_log, a_atan);
+      if (__double2hiint(r2) < P2P_SLOW_HI) {
+        if (r2 == 0.0) {
+          pr.lg = 0.0;
+          pr.ag = 0.0;
+          if (tv && !(self_mode && c0 + k == j)) atomicMin(bad, (unsigned long long)j);
+        } else {
+          pr.lg = 2.0 * log(hypot(dx, dy));
+          pr.ag = atan2(__dadd_rn(dy, 0.0), dx);
+        }
+      }
+      re = fma(s_u[k], pr.lg, re);
+      im = fma(s_u[k], pr.ag, im);
+    }
+  }
+  if (tv) phi[j] = make_double2(0.5 * re, im);
+}
+
 // debug hook: the P2P math on explicit (dx, dy) pairs -> (log |z|^2, Arg z)
 __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
                                  double2* __restrict__ out) {
@@ -510,6 +568,15 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
       default: return FMM_EBADCFG;
     }
   t->launches += 2;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+int fmm_direct_launch(const double* sxy, const double* su, int64_t n, const double* txy, int64_t m, int self_mode,
+                      const double* tabs, double* phi, unsigned long long* bad, cudaStream_t s) {
+  if (m > 0)
+    k_direct<<<(unsigned)((m + DIR_T - 1) / DIR_T), DIR_T, 0, s>>>((const double2*)sxy, su, n, (const double2*)txy, m,
+                                                                  self_mode, tabs, (double2*)phi, bad);
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }

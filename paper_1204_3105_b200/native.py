@@ -81,6 +81,7 @@ def lib():
             "fmm_launch_count": (C.c_int64, [vp]),
             "fmm_pool_reserve": (C.c_int, [C.c_size_t]),
             "fmm_tree_bytes": (C.c_size_t, [vp]),
+            "fmm_direct": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int32, vp, vp]),
             "fmm_free": (None, [vp]),
             "fmm_error_string": (C.c_char_p, [C.c_int]),
             "fmm_last_error_message": (C.c_char_p, []),
@@ -218,3 +219,21 @@ def pool_reserve(nbytes: int):
     rc = lib().fmm_pool_reserve(int(nbytes))
     if rc:
         raise FmmError(rc, "fmm_pool_reserve")
+
+
+def direct(src_xy, src_u, tgt_xy=None, self_mode=False, out=None, stream=None):
+    """fmm_direct: all-pairs Phi (complex128 [m]); torch CUDA tensor by default."""
+    n = int(src_u.shape[0])
+    m = n if self_mode else int(tgt_xy.shape[0])
+    if out is None:
+        import torch
+
+        out = torch.zeros(m, dtype=torch.complex128, device="cuda")
+    ps, ks = _ptr(src_xy)
+    pu, ku = _ptr(src_u)
+    pt, kt = _ptr(None if self_mode else tgt_xy)
+    po, ko = _ptr(out)
+    rc = lib().fmm_direct(ps, pu, n, pt, m, int(bool(self_mode)), po, _stream_ptr(stream))
+    if rc:
+        raise FmmError(rc, "fmm_direct")
+    return out

@@ -206,3 +206,34 @@ def test_heavy_blocks(n):
     g.check()
     ref = o.evaluate()
     assert normwise(phi, ref) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s"])
+def test_direct_sum_matches_oracle(name):
+    """fmm_direct (NEXT-1 reference) against the oracle's direct sum: same definition
+    (principal Log per pair, D13; i != j in self mode, D16), so Re and Im agree to rounding."""
+    import oracle
+
+    from paper_1204_3105_b200 import direct
+
+    w = SMALL_CASES["C1"] if name == "C1" else SMALL_CASES["C2"].scaled(6000, name="C2s")
+    d = data(w)
+    ref = oracle.direct(d["src_xy"], d["u"], d["tgt_xy"], self_mode=w.self_mode)
+    out = np.zeros(w.m, np.complex128)
+    direct(d["src_xy"], d["u"], d["tgt_xy"], self_mode=w.self_mode, out=out)
+    assert normwise(out, ref) <= 1e-14
+    import torch
+
+    dev = direct(torch.from_numpy(d["src_xy"]).cuda(), torch.from_numpy(d["u"]).cuda(),
+                 None if d["tgt_xy"] is None else torch.from_numpy(d["tgt_xy"]).cuda(), self_mode=w.self_mode)
+    assert np.array_equal(dev.cpu().numpy(), out)
+
+
+def test_direct_sum_coincident_raises():
+    from paper_1204_3105_b200 import FmmError, direct
+
+    src = np.array([[0.1, 0.2], [0.3, 0.4]])
+    tgt = np.array([[0.5, 0.5], [0.3, 0.4]])
+    with pytest.raises(FmmError) as e:
+        direct(src, np.ones(2), tgt, out=np.zeros(2, np.complex128))
+    assert e.value.code == 3
