@@ -179,6 +179,21 @@ int64_t fmm_launch_count(fmm_tree_t t);
 
 void fmm_free(fmm_tree_t t);
 
+/* Depth selection.  Cost of one build + evaluate at `depth`:
+ *   uc == NULL: the paper's appendix model (Table 2),
+ *     (M+N) p + K B/(B-1) (P4+2) p^2 + M (P2 N/K + p),  K = B^depth  (constant term dropped);
+ *   uc != NULL: a device-time model in the units of uc,
+ *     c0 + c_point (N+M)(p+1) + c_cell K B/(B-1) (P4+2) (p+1)^2 + c_pair M P2 N/K + c_leaf K,
+ * with (B, P4, P2) = (4, 27, 9) quadtree, (7, 42, 7) septree, (4, 39, 13) triangle-quadtree.
+ * fmm_choose_depth returns the depth of least cost (first minimum) in 1..10 (septree) or 1..15.
+ * Host only (no device work).  Errors: FMM_EBADCFG. */
+typedef struct {
+  double c0, c_point, c_cell, c_pair, c_leaf;
+} fmm_unit_costs;
+int fmm_predict_cost(int32_t tiling, int64_t n, int64_t m, int32_t p, int32_t depth, const fmm_unit_costs* uc,
+                     double* cost);
+int fmm_choose_depth(int32_t tiling, int64_t n, int64_t m, int32_t p, const fmm_unit_costs* uc, int32_t* depth);
+
 /* Direct evaluation (the reference of the paper's section-9 error and
  * runtime sweeps): phi_out[j] = sum_i src_u[i] Log(tgt_j - src_i) over all n
  * sources, O(n m), principal branch with a canonical +0 imaginary zero (D13); in self_mode

@@ -92,6 +92,8 @@ def lib():
             "orc_tree_evaluate": (C.c_int, [C.c_void_p, _i64, C.c_int64, _d, _i64, _i64]),
             "orc_tree_bound": (None, [C.c_void_p, _i64, C.c_int64, _d]),
             "orc_num_threads": (C.c_int, []),
+            "orc_paper_cost": (C.c_double, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
+            "orc_paper_depth": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -407,3 +409,12 @@ class Tree:
 
 def num_threads():
     return int(lib().orc_num_threads())
+
+
+def paper_cost(tiling, n, m, p, depth):
+    """appendix A-C cost model (NEXT-2), without the L-independent constant"""
+    return float(lib().orc_paper_cost(TILING[tiling], float(n), float(m), int(p), int(depth)))
+
+
+def paper_depth(tiling, n, m, p, maxdepth):
+    return int(lib().orc_paper_depth(TILING[tiling], float(n), float(m), int(p), int(maxdepth)))

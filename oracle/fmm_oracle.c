@@ -1180,3 +1180,40 @@ void orc_tree_bound(orc_tree* t, const int64_t* tgt_ids, int64_t ntgt, double* b
     bound[q] = Bj;
   }
 }
+
+/* ------------------------------------------------------------------ cost model (NEXT-2)
+ * Appendices A-C, eqs. app:quadbefore / app:sepbefore / app:tquadbefore:
+ *   cost(FMM) = (M + N) P + (K B/(B-1) (P4 + 2) - C0) P^2 + M (P2 s + P),
+ *   K = B^L leaves, s = N / K points per leaf, (B, P4, P2) = (4, 27, 9), (7, 42, 7), (4, 39, 13)
+ * (Table 2).  C0 does not depend on L (and is garbled for the triangle tree, reading
+ * D19), so it is left out: it does not move the minimum over L. */
+static void orc_cost_params(int tiling, double* B, double* P4, double* P2) {
+  if (tiling == ORC_QUAD) {
+    *B = 4.0; *P4 = 27.0; *P2 = 9.0;
+  } else if (tiling == ORC_SEPT) {
+    *B = 7.0; *P4 = 42.0; *P2 = 7.0;
+  } else {
+    *B = 4.0; *P4 = 39.0; *P2 = 13.0;
+  }
+}
+
+double orc_paper_cost(int tiling, double n, double m, int p, int depth) {
+  double B, P4, P2;
+  orc_cost_params(tiling, &B, &P4, &P2);
+  double K = pow(B, depth), s = n / K, P = (double)p;
+  return (m + n) * P + K * B / (B - 1.0) * (P4 + 2.0) * P * P + m * (P2 * s + P);
+}
+
+/* the depth 1..maxdepth of least paper cost (the first one on ties) */
+int orc_paper_depth(int tiling, double n, double m, int p, int maxdepth) {
+  int best = 1;
+  double bc = orc_paper_cost(tiling, n, m, p, 1);
+  for (int L = 2; L <= maxdepth; ++L) {
+    double c = orc_paper_cost(tiling, n, m, p, L);
+    if (c < bc) {
+      bc = c;
+      best = L;
+    }
+  }
+  return best;
+}

@@ -15,7 +15,10 @@ from .native import (  # noqa: F401
     QUADTREE,
     SEPTREE,
     TRIQUAD,
+    UnitCosts,
+    choose_depth,
     direct,
+    predict_cost,
 )
 
-__all__ = ["Config", "FmmError", "Tree", "X", "direct", "lib", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]
+__all__ = ["Config", "FmmError", "Tree", "UnitCosts", "X", "choose_depth", "direct", "lib", "predict_cost", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]

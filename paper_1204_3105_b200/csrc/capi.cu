@@ -269,6 +269,54 @@ int fmm_partition(const double* block_work, int64_t nblocks, int64_t leaves_per_
   return FMM_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-2: depth selection
+// The appendix cost model or a per-unit device-time model:
+//   paper: (M+N) P + K B/(B-1) (P4+2) P^2 + M (P2 s + P)          (s = N / K, K = B^L)
+//   unit : c0 + c_point (N+M)(p+1) + c_cell K B/(B-1) (P4+2) (p+1)^2 + c_pair M P2 s + c_leaf K
+static void cost_params(int tiling, double* B, double* P4, double* P2) {
+  if (tiling == FMM_QUADTREE) {
+    *B = 4.0; *P4 = 27.0; *P2 = 9.0;
+  } else if (tiling == FMM_SEPTREE) {
+    *B = 7.0; *P4 = 42.0; *P2 = 7.0;
+  } else {
+    *B = 4.0; *P4 = 39.0; *P2 = 13.0;
+  }
+}
+
+int fmm_predict_cost(int32_t tiling, int64_t n, int64_t m, int32_t p, int32_t depth, const fmm_unit_costs* uc,
+                     double* cost) {
+  if (tiling < 0 || tiling > 2 || n < 0 || m < 0 || p < 1 || depth < 1 || depth > 20 || !cost) return FMM_EBADCFG;
+  double B, P4, P2;
+  cost_params(tiling, &B, &P4, &P2);
+  const double K = pow(B, depth), N = (double)n, M = (double)m, s = N / K, P = (double)p;
+  if (!uc) {
+    *cost = (M + N) * P + K * B / (B - 1.0) * (P4 + 2.0) * P * P + M * (P2 * s + P);
+  } else {
+    const double P1 = P + 1.0;
+    *cost = uc->c0 + uc->c_point * (N + M) * P1 + uc->c_cell * K * B / (B - 1.0) * (P4 + 2.0) * P1 * P1 +
+            uc->c_pair * M * P2 * s + uc->c_leaf * K;
+  }
+  return FMM_OK;
+}
+
+int fmm_choose_depth(int32_t tiling, int64_t n, int64_t m, int32_t p, const fmm_unit_costs* uc, int32_t* depth) {
+  if (!depth) return FMM_EBADCFG;
+  const int maxd = tiling == FMM_SEPTREE ? 10 : 15;
+  int best = 1;
+  double bc = 0.0;
+  for (int L = 1; L <= maxd; ++L) {
+    double c;
+    int e = fmm_predict_cost(tiling, n, m, p, L, uc, &c);
+    if (e) return e;
+    if (L == 1 || c < bc) {
+      bc = c;
+      best = L;
+    }
+  }
+  *depth = best;
+  return FMM_OK;
+}
+
 int fmm_pool_reserve(size_t bytes) {
   init_pool_once();
   void* p = nullptr;

@@ -82,6 +82,9 @@ def lib():
             "fmm_pool_reserve": (C.c_int, [C.c_size_t]),
             "fmm_tree_bytes": (C.c_size_t, [vp]),
             "fmm_direct": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int32, vp, vp]),
+            "fmm_predict_cost": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int32, C.c_int32, vp,
+                                           P(C.c_double)]),
+            "fmm_choose_depth": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int32, vp, P(C.c_int32)]),
             "fmm_free": (None, [vp]),
             "fmm_error_string": (C.c_char_p, [C.c_int]),
             "fmm_last_error_message": (C.c_char_p, []),
@@ -237,3 +240,27 @@ def direct(src_xy, src_u, tgt_xy=None, self_mode=False, out=None, stream=None):
     if rc:
         raise FmmError(rc, "fmm_direct")
     return out
+
+
+class UnitCosts(C.Structure):
+    """fmm_unit_costs: device-time model coefficients (ms per unit)"""
+    _fields_ = [("c0", C.c_double), ("c_point", C.c_double), ("c_cell", C.c_double), ("c_pair", C.c_double),
+                ("c_leaf", C.c_double)]
+
+
+def predict_cost(tiling, n, m, p, depth, unit_costs=None):
+    out = C.c_double()
+    uc = None if unit_costs is None else C.byref(unit_costs)
+    rc = lib().fmm_predict_cost(_TILING[tiling], int(n), int(m), int(p), int(depth), uc, C.byref(out))
+    if rc:
+        raise FmmError(rc, "fmm_predict_cost")
+    return out.value
+
+
+def choose_depth(tiling, n, m, p, unit_costs=None):
+    out = C.c_int32()
+    uc = None if unit_costs is None else C.byref(unit_costs)
+    rc = lib().fmm_choose_depth(_TILING[tiling], int(n), int(m), int(p), uc, C.byref(out))
+    if rc:
+        raise FmmError(rc, "fmm_choose_depth")
+    return out.value
