@@ -50,7 +50,9 @@ void fmm_host_p2p_tables(double* tab) {
       long double t2 = dxneg ? PI - t1 : t1;
       long double t3 = dyneg ? -t2 : t2;
       tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k)] = (double)t3;
-      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = (double)k / P2P_ATAN_K;
+      // signed slope: tan(theta) (no swap) or -cot(theta) (swap), exactly +-k / K
+      const double sg = (swap ? -1.0 : 1.0) * ((dxneg ^ dyneg) ? -1.0 : 1.0);
+      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = sg * (double)k / P2P_ATAN_K;
     }
   }
 }

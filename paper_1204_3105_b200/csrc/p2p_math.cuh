@@ -12,7 +12,8 @@
 //            from a MUFU.RCP64H estimate; atan t = atan t_k + atan q,
 //            q = (num - t_k den) / (den + t_k num), |q| <= 1/128 + 2^-20;
 //            atan q = q - q^3/3 + q^5/5 - q^7/7 (truncation < 2^-62 |q|);
-//            the octant's offset and sign are folded into a table T[oct][k].
+//            the octant's reference angle and signed slope are tabulated per (oct, k), so
+//            that q = (P - tau Q) / (Q + tau P) carries the sign (no fix-up).
 //   division: MUFU.RCP64H estimate + one cubic Newton step (e + e^2), error ~ e^3.
 // Polynomial coefficients live in the constant bank (DFMA operands, no register moves).
 #pragma once
@@ -22,7 +23,7 @@
 #define P2P_TW 8  // targets per P2P warp task
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
 #define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
-// table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (T[oct][k], t_k), 8 x (K+1)
+// table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (theta[oct][k], tau[oct][k]), 8 x (K+1)
 #define P2P_TAB_LOG 0
 #define P2P_TAB_ATAN (2 * P2P_LOG_N)
 #define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * 8 * (P2P_ATAN_K + 1))
@@ -104,28 +105,25 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
 // so y - x never yields -0 there).
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
-  // t = min/max of |dx|, |dy| estimated with the MUFU reciprocal of the larger one (~2^-22)
-  // and rounded to k = round(64 t) by the 1.5 2^52 shift (FP64 pipe, no conversions)
-  const double ax = fabs(dx), ay = fabs(dy);
-  const bool swap = ay > ax;
-  const double num = swap ? ax : ay, den = swap ? ay : ax;
+  // Rotation by the reference direction theta of (octant, k): with (P, Q) = (dy, dx), or
+  // (-dx, dy) when |dy| > |dx|, and the table's signed slope tau (+-k/64; its sign folds the
+  // octant's orientation), Arg z = theta + atan(q), q = (P - tau Q) / (Q + tau P) -- no sign
+  // fix-up.  k = round(64 |P| / |Q|) from the MUFU reciprocal (~2^-22) and the 1.5 2^52 shift.
+  const bool swap = fabs(dy) > fabs(dx);
+  const double P = swap ? -dx : dy, Q = swap ? dy : dx;
   double r0;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(den));
-  const int k = __double2loint(fma(num * r0, (double)P2P_ATAN_K, 6755399441055744.0)) & 0x7f;  // 0..64
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(Q));
+  const int k = __double2loint(fma(fabs(P * r0), (double)P2P_ATAN_K, 6755399441055744.0)) & 0x7f;  // 0..64
   // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
   const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
-  const double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (T[oct][k], t_k)
-  double a = fma(-Tt.y, den, num);
-  double b = fma(Tt.y, num, den);
-  double q = a * p2p_rcp(b);
-  double q2 = q * q;
+  const double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (theta[oct][k], tau[oct][k])
+  const double a = fma(-Tt.y, Q, P);
+  const double b = fma(Tt.y, P, Q);
+  const double q = a * p2p_rcp(b);
+  const double q2 = q * q;
   // q^7 coefficient rounded to a 20-bit mantissa (immediate), error < 2^-62 |q|
-  double P = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
-  P = fma(P, q2, P2P_C[9]);  // -1/3
-  double at = fma(q * q2, P, q);
-  // sign S = (-1)^(swap + dxneg + dyneg) applied by flipping the sign bit
-  const int sgn = (hx ^ hy ^ (swap ? 0x80000000 : 0)) & 0x80000000;
-  at = __hiloint2double(__double2hiint(at) ^ sgn, __double2loint(at));
-  return Tt.x + at;
+  double Pq = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
+  Pq = fma(Pq, q2, P2P_C[9]);  // -1/3
+  return Tt.x + fma(q * q2, Pq, q);
 }
