@@ -50,15 +50,15 @@ WORKLOADS = {
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # SURVEY §8(d) algorithmic work per unit:
 #  * P2P: F_pair FP64 flops per near-field interaction (ordered target-source pair), measured by
-#    ncu on the one-pair-per-thread microbenchmark tools/fpair_micro.py: 47 flops of math
-#    (|z|^2, log|z|^2, Arg z) + 2 DADD (y - x) + 2 DFMA (strength products) = 53
-#    (profiles/r01/fp64_counts.json; 52 with the round's earlier 128-entry / 32-knot tables).  The symmetric self-mode kernel evaluates each unordered
+#    ncu on the one-pair-per-thread microbenchmark tools/fpair_micro.py: 46 flops of math
+#    (|z|^2, log|z|^2, Arg z) + 2 DADD (y - x) + 2 DFMA (strength products) = 52
+#    (profiles/r01/fp64_counts.json, re-measured after every change of the pair math).  The symmetric self-mode kernel evaluates each unordered
 #    pair once, so it executes fewer flops than this per interaction (reported beside it).
 #  * M2L: the dense-operator count 8 (p+1)^2 flops per M2L op.
-F_PAIR = 53.0
+F_PAIR = 52.0
 # FP64 flops k_p2p_pairs executes per interaction (ncu, sm__sass_thread_inst_executed_op_
 # {dfma,dadd,dmul}_pred_on; profiles/r01/fp64_counts.json), for the executed-rate line
-F_EXEC = {"C4q": 31.74, "C4s": 29.55, "C4t": 31.49}
+F_EXEC = {"C4q": 31.17, "C4s": 29.02, "C4t": 30.92}
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu --set full,
 # profiles/r01/ncu_p2p_<cfg>_v16.txt); C4 = mean over its three launches.  The writes are the
 # per-(target, near slot) partial sums (m x nslot x 16 B) that k_p2p_finish adds.
