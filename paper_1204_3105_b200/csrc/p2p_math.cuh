@@ -5,21 +5,22 @@
 // pair loop ~4x slower.  Valid for |z| >= 1e-30 (the caller sends
 // smaller |z|, including the excluded / coincident z = 0, to an exact slow path).
 //
-//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 256-entry table of
-//            (1/c_i, log c_i) selected by the top mantissa bits; |r| < 2^-8.4;
-//            log1p(r) by its Taylor series to r^6 (truncation < 2^-61 |r|).
+//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 512-entry table of
+//            (1/c_i, log c_i) selected by the top mantissa bits; |r| <= 2^-10;
+//            log1p(r) by its Taylor series to r^5 (truncation < 2^-62.5, < 2^-52.5 |r|).
 //   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/64 with k = round(64 t)
 //            from a MUFU.RCP64H estimate; atan t = atan t_k + atan q,
 //            q = (num - t_k den) / (den + t_k num), |q| <= 1/128 + 2^-20;
 //            atan q = q - q^3/3 + q^5/5 - q^7/7 (truncation < 2^-62 |q|);
 //            the octant's reference angle and signed slope are tabulated per (oct, k), so
 //            that q = (P - tau Q) / (Q + tau P) carries the sign (no fix-up).
-//   division: MUFU.RCP64H estimate + one cubic Newton step (e + e^2), error ~ e^3.
+//   division: q0 = a r0 from the MUFU.RCP64H estimate r0, q = q0 (1 + e + e^2), e = 1 - b r0,
+//            error ~ e^3.
 // Polynomial coefficients live in the constant bank (DFMA operands, no register moves).
 #pragma once
 #include <stdint.h>
 
-#define P2P_LOG_N 256
+#define P2P_LOG_N 512
 #define P2P_TW 8  // targets per P2P warp task
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
 #define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
@@ -29,11 +30,11 @@
 #define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * 8 * (P2P_ATAN_K + 1))
 // |z|^2 below this (hi word of 1e-60) takes the exact slow path
 #define P2P_SLOW_HI 0x3379b604
-// z intervals: bit patterns [OFF + i 2^44, OFF + (i+1) 2^44), OFF = 0x3fe6000000000000 - 2^43,
-// so that the bit pattern of 1.0 is the centre of interval 160
-#define P2P_LOG_OFF_HI 0x3fe5f800
-#define P2P_LOG_OFF 0x3fe5f80000000000ull
-#define P2P_LOG_SHIFT 44
+// z intervals: bit patterns [OFF + i 2^43, OFF + (i+1) 2^43), OFF = 0x3fe6000000000000 - 2^42,
+// so that the bit pattern of 1.0 is the centre of interval 320
+#define P2P_LOG_OFF_HI 0x3fe5fc00
+#define P2P_LOG_OFF 0x3fe5fc0000000000ull
+#define P2P_LOG_SHIFT 43
 
 __constant__ double P2P_C[13] = {
     1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,  // log1p Taylor r^7 .. r^2
@@ -85,10 +86,9 @@ __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double
   const double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
-  // r^5, r^6 coefficients rounded to 20-bit mantissas (SASS immediates): their error
-  // (< 2^-21 relative) times r^n/n stays below 2^-62 for |r| <= 2^-8.4
-  double q = fma(r, -0x1.5555500000000p-3 /* ~-1/6 */, 0x1.9999900000000p-3 /* ~1/5 */);
-  q = fma(q, r, -0.25);
+  // r^5 coefficient rounded to a 20-bit mantissa (SASS immediate): its error
+  // (< 2^-21 relative) times r^5/5 stays below 2^-70 for |r| <= 2^-10
+  double q = fma(r, 0x1.9999900000000p-3 /* ~1/5 */, -0.25);
   q = fma(q, r, P2P_C[4]);  // 1/3 (full precision)
   q = fma(q, r, -0.5);
   *lz = cl.y + fma(r_2, q, r);  // log c_i + log1p(r)
@@ -120,7 +120,13 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   const double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (theta[oct][k], tau[oct][k])
   const double a = fma(-Tt.y, Q, P);
   const double b = fma(Tt.y, P, Q);
-  const double q = a * p2p_rcp(b);
+  // q = a / b: q0 = a r0 beside the residual e = 1 - b r0, then q0 (1 + e + e^2)
+  double r1;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r1) : "d"(b));
+  const double q0 = a * r1;
+  double e = fma(-b, r1, 1.0);
+  e = fma(e, e, e);
+  const double q = fma(q0, e, q0);
   const double q2 = q * q;
   // q^7 coefficient rounded to a 20-bit mantissa (immediate), error < 2^-62 |q|
   double Pq = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
