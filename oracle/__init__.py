@@ -94,6 +94,8 @@ def lib():
             "orc_num_threads": (C.c_int, []),
             "orc_paper_cost": (C.c_double, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
             "orc_paper_depth": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
+            "orc_draw": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+            "orc_sample_cells": (C.c_int, [cfgp, _i64, C.c_int64, C.c_int32, C.c_uint64, C.c_int64, _d, _d]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -418,3 +420,28 @@ def paper_cost(tiling, n, m, p, depth):
 
 def paper_depth(tiling, n, m, p, maxdepth):
     return int(lib().orc_paper_depth(TILING[tiling], float(n), float(m), int(p), int(maxdepth)))
+
+
+def draw(seed, counter):
+    """counter-based draw h(seed, counter) of the NEXT-4 sampler (D22)"""
+    return int(lib().orc_draw(C.c_uint64(seed), C.c_uint64(counter)))
+
+
+def sample_cells(cfg, cells, per_cell, seed, first=0, want_u=True):
+    """NEXT-4 regular-polygon point picking (Fig. 12; D22): per_cell points in each
+    leaf of `cells` (None: leaves 0..K-1) -> (xy (n, 2), u (n,) or None)"""
+    if cells is None:
+        ncells = int(lib().orc_num_cells(C.byref(cfg), cfg.depth))
+        cp = None
+    else:
+        cells = np.ascontiguousarray(cells, np.int64)
+        ncells = len(cells)
+        cp = _ptr(cells, _i64)
+    n = ncells * int(per_cell)
+    xy = np.zeros((n, 2))
+    u = np.zeros(n) if want_u else None
+    rc = lib().orc_sample_cells(C.byref(cfg), cp, ncells, int(per_cell), C.c_uint64(seed), int(first),
+                                _ptr(xy, _d), _ptr(u, _d) if want_u else None)
+    if rc:
+        raise OracleError(rc)
+    return xy, u

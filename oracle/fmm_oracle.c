@@ -1217,3 +1217,91 @@ int orc_paper_depth(int tiling, double n, double m, int p, int maxdepth) {
   }
   return best;
 }
+
+/* ======================================================================
+ * 7. NEXT-4: regular-polygon point picking (Fig. 12; reading D22)
+ *
+ * "the polygon is subdivided into disjoint isosceles triangles per edge where halves of
+ * triangles are rearranged to form rectangles.  Uniformly random points (x,y) are picked
+ * from this rectangle and a third uniformly random variable z assigns the point to one of
+ * the isosceles triangles".  The random numbers are counter-based (D22): draw d of
+ * point g is h(seed, 4g + d), the SplitMix64 output after 4g + d + 1 increments of the
+ * state `seed`, so any point can be drawn alone (sampled parity checks, rank slices).
+ * ====================================================================== */
+uint64_t orc_draw(uint64_t seed, uint64_t counter) {
+  uint64_t z = seed + (counter + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static double unit53(uint64_t h) { return (double)(h >> 11) * 0x1p-53; } /* [0, 1), 53 bits */
+
+/* cos and sin of k pi / 6, k = 0..11, exact where the value is 0, 1/2 or 1 (H otherwise) */
+static void dir_pi6(int k, double* c, double* s) {
+  static const double C[12] = {1.0, H, 0.5, 0.0, -0.5, -H, -1.0, -H, -0.5, 0.0, 0.5, H};
+  *c = C[k % 12];
+  *s = C[(k + 9) % 12]; /* sin(k pi/6) = cos((k - 3) pi/6) */
+}
+
+int orc_sample_cells(const orc_config* c, const int64_t* cells, int64_t ncells, int32_t per_cell, uint64_t seed,
+                     int64_t first, double* xy, double* u) {
+  const int L = c->depth;
+  const int64_t K = ipow(c->tiling == ORC_SEPT ? 7 : 4, L);
+  /* polygon of a leaf: nsides, half-edge a, apothem b (the rectangle is a x b) */
+  int nsides;
+  double a, b;
+  if (c->tiling == ORC_QUAD) { /* square of side S 2^-L */
+    nsides = 4;
+    a = 0.5 * ldexp(c->root_size, -L);
+    b = a;
+  } else if (c->tiling == ORC_SEPT) { /* hexagon of circumradius r (D8), a vertex at angle 0 */
+    nsides = 6;
+    double r = sept_leaf_r(c);
+    a = 0.5 * r;
+    b = H * r;
+  } else { /* triangle of circumradius R0 2^-L, upright or inverted (isUp) */
+    nsides = 3;
+    double R = ldexp(c->root_size, -L);
+    a = H * R;
+    b = 0.5 * R;
+  }
+  for (int64_t i = 0; i < ncells; ++i) {
+    int64_t cell = cells ? cells[i] : i;
+    if (cell < 0 || cell >= K) return ORC_EDOMAIN;
+    double cen[2];
+    orc_cell_center(c, L, cell, cen);
+    /* apothem direction of edge z, in units of pi/6:
+     *   quad 3z (edges facing 0, pi/2, pi, 3pi/2), hexagon 2z + 1 (pi/6 + z pi/3),
+     *   upright triangle 4z + 1 (pi/6, 5pi/6, 3pi/2), inverted 4z + 3 (pi/2, 7pi/6, 11pi/6) */
+    int step = c->tiling == ORC_QUAD ? 3 : (c->tiling == ORC_SEPT ? 2 : 4);
+    int off = c->tiling == ORC_QUAD ? 0 : (c->tiling == ORC_SEPT ? 1 : (orc_triq_isup(cell, L, L) > 0 ? 1 : 3));
+    for (int32_t j = 0; j < per_cell; ++j) {
+      const int64_t o = i * per_cell + j;
+      const uint64_t g = (uint64_t)(first + o);
+      const double s = unit53(orc_draw(seed, 4 * g + 0));
+      const double t = unit53(orc_draw(seed, 4 * g + 1));
+      const int z = (int)(((orc_draw(seed, 4 * g + 2) >> 32) * (uint64_t)nsides) >> 32);
+      /* rectangle [0, a] x [0, b]: the half s <= t is the right half of the isosceles
+       * triangle (X along the edge, Y along the apothem), the half s > t is moved onto its
+       * left half */
+      double X, Y;
+      if (s > t) {
+        X = (s - 1.0) * a;
+        Y = (1.0 - t) * b;
+      } else {
+        X = s * a;
+        Y = t * b;
+      }
+      double cs, sn;
+      dir_pi6(step * z + off, &cs, &sn);
+      /* rotate: +Y along the apothem direction (cs, sn), +X along (sn, -cs) */
+      const double px = Y * cs + X * sn;
+      const double py = Y * sn - X * cs;
+      xy[2 * o] = cen[0] + px;
+      xy[2 * o + 1] = cen[1] + py;
+      if (u) u[o] = 2.0 * unit53(orc_draw(seed, 4 * g + 3)) - 1.0;
+    }
+  }
+  return ORC_OK;
+}

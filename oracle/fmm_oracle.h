@@ -127,6 +127,15 @@ int orc_num_threads(void);
 double orc_paper_cost(int tiling, double n, double m, int p, int depth);
 int orc_paper_depth(int tiling, double n, double m, int p, int maxdepth);
 
+/* NEXT-4: regular-polygon point picking in leaf cells (Fig. 12; reading D22).
+ * Point g = first + i*per_cell + j (i < ncells, j < per_cell) is drawn uniformly in the leaf
+ * polygon of cells[i] (cells == NULL: cell i) from the counter-based draws h(seed, 4g + d),
+ * d = 0..3 (s, t, z, strength); xy[2(i*per_cell+j)..] = (x, y), u[...] = strength in [-1, 1)
+ * (u may be NULL).  Returns ORC_EDOMAIN when a cell is outside [0, B^L). */
+uint64_t orc_draw(uint64_t seed, uint64_t counter);
+int orc_sample_cells(const orc_config* c, const int64_t* cells, int64_t ncells, int32_t per_cell, uint64_t seed,
+                     int64_t first, double* xy, double* u);
+
 #ifdef __cplusplus
 }
 #endif
