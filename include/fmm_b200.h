@@ -204,6 +204,25 @@ int fmm_choose_depth(int32_t tiling, int64_t n, int64_t m, int32_t p, const fmm_
 int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const double* tgt_xy, int64_t m,
                int32_t self_mode, double* phi_out, void* stream);
 
+/* Device-side input generation: regular-polygon point picking in
+ * leaf cells, PAPER.md P:426-433 and Fig. 12 -- the leaf polygon is cut into one isosceles
+ * triangle per edge, halves of each triangle are rearranged into an a x b rectangle
+ * (half-edge x apothem), (s, t) is uniform in the rectangle and z uniform in the edges.
+ * Leaf polygons: square of side root_size 2^-L; hexagon of circumradius r (D8) with a vertex
+ * at angle 0; triangle of circumradius root_size 2^-L, upright or inverted (isUp);
+ * centred at CellCenter of the leaf (D12).
+ *
+ * Point o (0 <= o < ncells * per_cell) lies in leaf cells[o / per_cell] (cells == NULL: leaf
+ * o / per_cell, ncells <= B^L) and is point g = first + o of the sample: its draws are the
+ * counter-based SplitMix64 outputs h(seed, 4g + d), d = 0..3 (reading D22), so that a rank
+ * or a check can generate any slice alone.  xy: device, interleaved (x, y) float64 pairs,
+ * ncells * per_cell of them; u: device strengths 2 h_3 2^-53 - 1 in [-1, 1), or NULL;
+ * cells: device int64 or NULL.  Bit-identical to the oracle's sampler (every rounding fixed).
+ * Synchronises `stream`.  Errors: FMM_EBADCFG (config, sizes, host pointers),
+ * FMM_EDOMAIN (a cell outside [0, B^L); message names the smallest cells index). */
+int fmm_sample_cells(const fmm_config* cfg, const int64_t* cells, int64_t ncells, int32_t per_cell, uint64_t seed,
+                     int64_t first, double* xy, double* u, void* stream);
+
 /* Test hook: the P2P kernel's FP64 math on n explicit offsets z = dx + i dy (device
  * pointers, interleaved): out[2i] = log|z|^2, out[2i+1] = Arg z in (-pi, pi] with a zero
  * imaginary part read as +0 (D13).  z must have a normal |z|^2 (the kernel

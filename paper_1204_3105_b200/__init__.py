@@ -19,6 +19,7 @@ from .native import (  # noqa: F401
     choose_depth,
     direct,
     predict_cost,
+    sample_cells,
 )
 
-__all__ = ["Config", "FmmError", "Tree", "UnitCosts", "X", "choose_depth", "direct", "lib", "predict_cost", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]
+__all__ = ["Config", "FmmError", "Tree", "UnitCosts", "X", "choose_depth", "direct", "lib", "predict_cost", "sample_cells", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]

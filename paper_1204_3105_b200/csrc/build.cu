@@ -8,8 +8,6 @@
 #include "fmm_internal.cuh"
 #include "geometry.cuh"
 
-namespace {
-
 DGeo dgeo(const Geo& g) {
   DGeo d;
   d.tiling = g.tiling;
@@ -24,6 +22,8 @@ DGeo dgeo(const Geo& g) {
   d.sept_D3r = g.sept_D3r;
   return d;
 }
+
+namespace {
 
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)

@@ -589,6 +589,50 @@ int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const doubl
   return FMM_OK;
 }
 
+int fmm_sample_cells(const fmm_config* cfg, const int64_t* cells, int64_t ncells, int32_t per_cell, uint64_t seed,
+                     int64_t first, double* xy, double* u, void* stream) {
+  Geo g;
+  int e = make_geo(cfg, &g);
+  if (e) return e;
+  if (ncells < 0 || per_cell < 0 || first < 0) return FMM_EBADCFG;
+  if (!cells && ncells > g.K) return FMM_EBADCFG;
+  if (per_cell > 0 && ncells > (((int64_t)1 << 60) - first) / per_cell) return FMM_EBADCFG;
+  const int64_t npts = ncells * (int64_t)per_cell;
+  if (npts == 0) return FMM_OK;
+  if (!is_device_ptr(xy) || (u && !is_device_ptr(u)) || (cells && !is_device_ptr(cells))) return FMM_EBADCFG;
+  // leaf polygon (D22): half-edge a and apothem b of the rectangle, apothem directions
+  SamplePoly P;
+  if (g.tiling == FMM_QUADTREE) {  // square of side S 2^-L; edges facing 0, pi/2, pi, 3pi/2
+    P.nsides = 4, P.step = 3, P.off = 0;
+    P.a = 0.5 * ldexp(g.root_size, -g.L);
+    P.b = P.a;
+  } else if (g.tiling == FMM_SEPTREE) {  // hexagon of circumradius r (D8), a vertex at angle 0
+    P.nsides = 6, P.step = 2, P.off = 1;
+    P.a = 0.5 * g.sept_r;
+    P.b = 0.8660254037844386 * g.sept_r;
+  } else {  // triangle of circumradius R0 2^-L; off (1 upright, 3 inverted) per cell
+    const double R = ldexp(g.root_size, -g.L);
+    P.nsides = 3, P.step = 4, P.off = 1;
+    P.a = 0.8660254037844386 * R;
+    P.b = 0.5 * R;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* dbad = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&dbad, 8, s));
+  FMM_CUDA_TRY(cudaMemsetAsync(dbad, 0xff, 8, s));
+  e = fmm_sample_launch(g, cells, ncells, per_cell, seed, first, P, xy, u, dbad, s);
+  unsigned long long bad = ~0ull;
+  if (!e) FMM_CUDA_TRY(cudaMemcpyAsync(&bad, dbad, 8, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(dbad, s);
+  if (e) return e;
+  if (bad != ~0ull) {
+    fmm_set_error_message("cell outside [0, B^L) at cells index " + std::to_string(bad));
+    return FMM_EDOMAIN;
+  }
+  return FMM_OK;
+}
+
 int fmm_debug_p2p_math(const double* dxdy, int64_t n, double* out, void* stream) {
   if (n <= 0) return FMM_OK;
   if (!is_device_ptr(dxdy) || !is_device_ptr(out)) return FMM_EBADCFG;

@@ -116,6 +116,17 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi_out);
 int fmm_build_tasks(fmm_tree_s* t);
 int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);
 int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s);
+// build.cu: the device geometry of a tree (geometry.cuh)
+struct DGeo;
+DGeo dgeo(const Geo& g);
+// sample.cu (NEXT-4): leaf polygon of the regular-polygon point picking (D22):
+// nsides, half-edge a, apothem b; apothem direction of edge z = (step z + off) pi / 6
+struct SamplePoly {
+  int nsides, step, off;
+  double a, b;
+};
+int fmm_sample_launch(const Geo& G, const int64_t* cells, int64_t ncells, int per_cell, uint64_t seed, int64_t first,
+                      const SamplePoly& P, double* xy, double* u, unsigned long long* bad, cudaStream_t s);
 // capi.cu
 void fmm_host_p2p_tables(double* tab);  // fills P2P_TAB_DOUBLES doubles
 int fmm_direct_launch(const double* sxy, const double* su, int64_t n, const double* txy, int64_t m, int self_mode,

@@ -1,0 +1,86 @@
+// sample.cu -- SURVEY §8(f) NEXT-4: device-side input generation.  Regular-polygon point
+// picking in leaf cells (Fig. 12): "the polygon is subdivided into
+// disjoint isosceles triangles per edge where halves of triangles are rearranged to form
+// rectangles.  Uniformly random points (x,y) are picked from this rectangle and a third
+// uniformly random variable z assigns the point to one of the isosceles triangles."
+//
+// Random numbers are counter-based (reading D22): draw d of point g is the
+// SplitMix64 output h(seed, 4g + d), so a point depends only on (seed, g) -- any slice of a
+// sample (a rank's cells, a sampled check) is drawn alone.  The leaf polygon comes from the
+// tree's own geometry: centre by CellCenter (geometry.cuh, bit-exact form D12), the
+// triangle's orientation by the parity of its centre-child digits (isUp), and
+// every rounding is an explicit __d*_rn so that the points are bit-identical to the oracle's.
+#include <algorithm>
+
+#include "fmm_internal.cuh"
+#include "geometry.cuh"
+
+namespace {
+
+__device__ __forceinline__ uint64_t smix_draw(uint64_t seed, uint64_t counter) {
+  uint64_t z = seed + (counter + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double unit53(uint64_t h) { return __dmul_rn((double)(h >> 11), 0x1p-53); }
+
+// cos (k pi / 6), k = 0..11 (sin (k pi / 6) = entry (k + 9) mod 12)
+__constant__ double SMP_COS[12] = {1.0, FMM_H, 0.5, 0.0, -0.5, -FMM_H, -1.0, -FMM_H, -0.5, 0.0, 0.5, FMM_H};
+
+// one thread per point; point o of the call is point g = first + o of the sample
+__global__ void __launch_bounds__(256) k_sample_cells(DGeo g, const int64_t* __restrict__ cells, int64_t ncells,
+                                                      int per_cell, uint64_t seed, int64_t first, SamplePoly P,
+                                                      double2* __restrict__ xy, double* __restrict__ u,
+                                                      unsigned long long* bad) {
+  const int64_t npts = ncells * per_cell;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < npts; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = o / per_cell;
+    const int64_t cell = cells ? cells[i] : i;
+    if (cell < 0 || cell >= g.K) {
+      atomicMin(bad, (unsigned long long)i);
+      continue;
+    }
+    const double2 c = geo_centre(g, g.L, cell);
+    int off = P.off;
+    if (g.tiling == FMM_TRIQUAD) {  // inverted (an odd number of centre-child digits): 4z + 3
+      int zeros = 0;
+      for (int d = 0; d < g.L; ++d) zeros += ((cell >> (2 * d)) & 3) == 0;
+      off = (zeros & 1) ? 3 : 1;
+    }
+    const uint64_t gi = (uint64_t)(first + o);
+    const double s = unit53(smix_draw(seed, 4 * gi)), t = unit53(smix_draw(seed, 4 * gi + 1));
+    const int z = (int)(((smix_draw(seed, 4 * gi + 2) >> 32) * (uint64_t)P.nsides) >> 32);
+    // rectangle a x b: s <= t is the right half of edge z's isosceles triangle, s > t its left half
+    double X, Y;
+    if (s > t) {
+      X = __dmul_rn(__dsub_rn(s, 1.0), P.a);
+      Y = __dmul_rn(__dsub_rn(1.0, t), P.b);
+    } else {
+      X = __dmul_rn(s, P.a);
+      Y = __dmul_rn(t, P.b);
+    }
+    const int k = P.step * z + off;
+    const double cs = SMP_COS[k % 12], sn = SMP_COS[(k + 9) % 12];
+    // +Y along the apothem direction (cs, sn), +X along the edge (sn, -cs)
+    const double px = __dadd_rn(__dmul_rn(Y, cs), __dmul_rn(X, sn));
+    const double py = __dsub_rn(__dmul_rn(Y, sn), __dmul_rn(X, cs));
+    xy[o] = make_double2(__dadd_rn(c.x, px), __dadd_rn(c.y, py));
+    if (u) u[o] = __dsub_rn(__dmul_rn(2.0, unit53(smix_draw(seed, 4 * gi + 3))), 1.0);
+  }
+}
+
+}  // namespace
+
+int fmm_sample_launch(const Geo& G, const int64_t* cells, int64_t ncells, int per_cell, uint64_t seed, int64_t first,
+                      const SamplePoly& P, double* xy, double* u, unsigned long long* bad, cudaStream_t s) {
+  const int64_t npts = ncells * per_cell;
+  if (npts > 0) {
+    const int64_t blocks = std::min<int64_t>((npts + 255) / 256, 148 * 64);
+    k_sample_cells<<<(unsigned)blocks, 256, 0, s>>>(dgeo(G), cells, ncells, per_cell, seed, first, P, (double2*)xy,
+                                                    u, bad);
+  }
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}

@@ -82,6 +82,7 @@ def lib():
             "fmm_pool_reserve": (C.c_int, [C.c_size_t]),
             "fmm_tree_bytes": (C.c_size_t, [vp]),
             "fmm_direct": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int32, vp, vp]),
+            "fmm_sample_cells": (C.c_int, [P(Config), vp, C.c_int64, C.c_int32, C.c_uint64, C.c_int64, vp, vp, vp]),
             "fmm_predict_cost": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int32, C.c_int32, vp,
                                            P(C.c_double)]),
             "fmm_choose_depth": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int32, vp, P(C.c_int32)]),
@@ -240,6 +241,36 @@ def direct(src_xy, src_u, tgt_xy=None, self_mode=False, out=None, stream=None):
     if rc:
         raise FmmError(rc, "fmm_direct")
     return out
+
+
+def sample_cells(cfg, cells, per_cell, seed, first=0, want_u=True, ncells=None, stream=None):
+    """fmm_sample_cells (NEXT-4, Fig. 12): per_cell uniform points in each leaf of
+    `cells` (int64 CUDA tensor; None: leaves 0..ncells-1) -> (xy float64 [n, 2], u float64 [n]
+    or None), CUDA tensors."""
+    import torch
+
+    if cells is not None:
+        if not (hasattr(cells, "is_cuda") and cells.is_cuda and cells.dtype == torch.int64):
+            raise TypeError("cells must be an int64 CUDA tensor")
+        ncells = int(cells.shape[0])
+    elif ncells is None:
+        ncells = int(cfg_leaves(cfg))
+    n = ncells * int(per_cell)
+    xy = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    u = torch.empty(n, dtype=torch.float64, device="cuda") if want_u else None
+    pc, kc = _ptr(cells)
+    px, kx = _ptr(xy)
+    pu, ku = _ptr(u)
+    rc = lib().fmm_sample_cells(C.byref(cfg), pc, ncells, int(per_cell), C.c_uint64(seed), int(first), px, pu,
+                                _stream_ptr(stream))
+    if rc:
+        raise FmmError(rc, "fmm_sample_cells")
+    return xy, u
+
+
+def cfg_leaves(cfg):
+    """B^L leaves of a Config"""
+    return (7 if cfg.tiling == SEPTREE else 4) ** int(cfg.depth)
 
 
 class UnitCosts(C.Structure):
