@@ -547,6 +547,7 @@ int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const doubl
   if (n < 0 || m < 0 || (self_mode && m != n)) return FMM_EBADCFG;
   if (m == 0) return FMM_OK;
   if (!phi_out || (n > 0 && (!src_xy || !src_u)) || (!self_mode && !tgt_xy)) return FMM_EBADCFG;
+  init_pool_once();
   cudaStream_t s = (cudaStream_t)stream;
   // device copies of host inputs / output, the P2P tables and the error word in one allocation
   const bool dsx = is_device_ptr(src_xy), dsu = is_device_ptr(src_u), dphi = is_device_ptr(phi_out);
@@ -616,6 +617,7 @@ int fmm_sample_cells(const fmm_config* cfg, const int64_t* cells, int64_t ncells
     P.a = 0.8660254037844386 * R;
     P.b = 0.5 * R;
   }
+  init_pool_once();
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* dbad = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync((void**)&dbad, 8, s));

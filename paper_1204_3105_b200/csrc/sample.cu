@@ -29,26 +29,44 @@ __device__ __forceinline__ double unit53(uint64_t h) { return __dmul_rn((double)
 // cos (k pi / 6), k = 0..11 (sin (k pi / 6) = entry (k + 9) mod 12)
 __constant__ double SMP_COS[12] = {1.0, FMM_H, 0.5, 0.0, -0.5, -FMM_H, -1.0, -FMM_H, -0.5, 0.0, 0.5, FMM_H};
 
-// one thread per point; point o of the call is point g = first + o of the sample
-__global__ void __launch_bounds__(256) k_sample_cells(DGeo g, const int64_t* __restrict__ cells, int64_t ncells,
-                                                      int per_cell, uint64_t seed, int64_t first, SamplePoly P,
-                                                      double2* __restrict__ xy, double* __restrict__ u,
-                                                      unsigned long long* bad) {
+// one thread per point, 256-point tiles; the leaf polygons a tile touches (<= 256) are
+// placed first, one per thread, in shared memory (centre, apothem-direction offset); point o
+// of the call is point g = first + o of the sample
+constexpr int SMP_T = 256;
+__global__ void __launch_bounds__(SMP_T) k_sample_cells(DGeo g, const int64_t* __restrict__ cells, int64_t ncells,
+                                                        int per_cell, uint64_t seed, int64_t first, SamplePoly P,
+                                                        double2* __restrict__ xy, double* __restrict__ u,
+                                                        unsigned long long* bad) {
+  __shared__ double2 s_cen[SMP_T];
+  __shared__ int s_off[SMP_T];
   const int64_t npts = ncells * per_cell;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < npts; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = o / per_cell;
-    const int64_t cell = cells ? cells[i] : i;
-    if (cell < 0 || cell >= g.K) {
-      atomicMin(bad, (unsigned long long)i);
-      continue;
+  for (int64_t o0 = blockIdx.x * (int64_t)SMP_T; o0 < npts; o0 += (int64_t)gridDim.x * SMP_T) {
+    const int64_t i0 = o0 / per_cell;
+    const int nc = (int)((min(o0 + SMP_T, npts) - 1) / per_cell - i0 + 1);
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      const int64_t cell = cells ? cells[i0 + threadIdx.x] : i0 + threadIdx.x;
+      int off = -1;
+      if (cell < 0 || cell >= g.K) {
+        atomicMin(bad, (unsigned long long)(i0 + threadIdx.x));
+      } else {
+        s_cen[threadIdx.x] = geo_centre(g, g.L, cell);
+        off = P.off;
+        if (g.tiling == FMM_TRIQUAD) {  // inverted (an odd number of centre-child digits): 4z + 3
+          int zeros = 0;
+          for (int d = 0; d < g.L; ++d) zeros += ((cell >> (2 * d)) & 3) == 0;
+          off = (zeros & 1) ? 3 : 1;
+        }
+      }
+      s_off[threadIdx.x] = off;
     }
-    const double2 c = geo_centre(g, g.L, cell);
-    int off = P.off;
-    if (g.tiling == FMM_TRIQUAD) {  // inverted (an odd number of centre-child digits): 4z + 3
-      int zeros = 0;
-      for (int d = 0; d < g.L; ++d) zeros += ((cell >> (2 * d)) & 3) == 0;
-      off = (zeros & 1) ? 3 : 1;
-    }
+    __syncthreads();
+    const int64_t o = o0 + threadIdx.x;
+    if (o >= npts) continue;
+    const int q = (int)((uint32_t)(o - i0 * per_cell) / (uint32_t)per_cell);
+    const int off = s_off[q];
+    if (off < 0) continue;
+    const double2 c = s_cen[q];
     const uint64_t gi = (uint64_t)(first + o);
     const double s = unit53(smix_draw(seed, 4 * gi)), t = unit53(smix_draw(seed, 4 * gi + 1));
     const int z = (int)(((smix_draw(seed, 4 * gi + 2) >> 32) * (uint64_t)P.nsides) >> 32);
@@ -77,8 +95,8 @@ int fmm_sample_launch(const Geo& G, const int64_t* cells, int64_t ncells, int pe
                       const SamplePoly& P, double* xy, double* u, unsigned long long* bad, cudaStream_t s) {
   const int64_t npts = ncells * per_cell;
   if (npts > 0) {
-    const int64_t blocks = std::min<int64_t>((npts + 255) / 256, 148 * 64);
-    k_sample_cells<<<(unsigned)blocks, 256, 0, s>>>(dgeo(G), cells, ncells, per_cell, seed, first, P, (double2*)xy,
+    const int64_t blocks = std::min<int64_t>((npts + SMP_T - 1) / SMP_T, 148 * 8 * 16);
+    k_sample_cells<<<(unsigned)blocks, SMP_T, 0, s>>>(dgeo(G), cells, ncells, per_cell, seed, first, P, (double2*)xy,
                                                     u, bad);
   }
   FMM_CUDA_TRY(cudaGetLastError());

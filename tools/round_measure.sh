@@ -11,3 +11,6 @@ for c in C4s C4t; do
   ncu --set full --clock-control none --import-source on -k regex:k_p2p_pairs -c 1 -o gpurun_out/p2p_full_$c \
       python tools/profile_one.py $c 1 >> gpurun_out/full_$c.log 2>&1
 done
+python tools/sample_bench.py > gpurun_out/sample_$R.jsonl 2> gpurun_out/sample_$R.err &&
+ncu --set full --clock-control none --import-source on -k regex:k_sample_cells -c 3 -o gpurun_out/sample_full_$R \
+    python tools/sample_bench.py 1 > gpurun_out/sample_ncu_$R.log 2>&1
