@@ -26,8 +26,9 @@ __device__ __forceinline__ uint64_t smix_draw(uint64_t seed, uint64_t counter) {
 
 __device__ __forceinline__ double unit53(uint64_t h) { return __dmul_rn((double)(h >> 11), 0x1p-53); }
 
-// cos (k pi / 6), k = 0..11 (sin (k pi / 6) = entry (k + 9) mod 12)
-__constant__ double SMP_COS[12] = {1.0, FMM_H, 0.5, 0.0, -0.5, -FMM_H, -1.0, -FMM_H, -0.5, 0.0, 0.5, FMM_H};
+// cos (k pi / 6), k = 0..20 (sin (k pi / 6) = entry k + 9; apothem directions have k <= 11)
+__constant__ double SMP_COS[21] = {1.0,  FMM_H, 0.5, 0.0, -0.5, -FMM_H, -1.0, -FMM_H, -0.5, 0.0, 0.5,
+                                   FMM_H, 1.0,  FMM_H, 0.5, 0.0,  -0.5,  -FMM_H, -1.0, -FMM_H, -0.5};
 
 // one thread per point, 256-point tiles; the leaf polygons a tile touches (<= 256) are
 // placed first, one per thread, in shared memory (centre, apothem-direction offset); point o
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(SMP_T) k_sample_cells(DGeo g, const int64_t* _
       Y = __dmul_rn(t, P.b);
     }
     const int k = P.step * z + off;
-    const double cs = SMP_COS[k % 12], sn = SMP_COS[(k + 9) % 12];
+    const double cs = SMP_COS[k], sn = SMP_COS[k + 9];  // k = step z + off <= 11
     // +Y along the apothem direction (cs, sn), +X along the edge (sn, -cs)
     const double px = __dadd_rn(__dmul_rn(Y, cs), __dmul_rn(X, sn));
     const double py = __dsub_rn(__dmul_rn(Y, sn), __dmul_rn(X, cs));
