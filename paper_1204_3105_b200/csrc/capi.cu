@@ -32,6 +32,7 @@ std::vector<double> host_binom() {
 
 // tables of p2p_math.cuh, computed once in extended precision (x87 long double)
 void fmm_host_p2p_tables(double* tab) {
+  memset(tab, 0, sizeof(double) * P2P_TAB_DOUBLES);  // unused atan slots k = 65..127 read as 0
   for (int i = 0; i < P2P_LOG_N; ++i) {
     // interval centre: the value of the centre bit pattern (exactly 1.0 for the interval of 1.0)
     uint64_t mid = P2P_LOG_OFF + ((uint64_t)i << P2P_LOG_SHIFT) + ((uint64_t)1 << (P2P_LOG_SHIFT - 1));
@@ -49,10 +50,10 @@ void fmm_host_p2p_tables(double* tab) {
       long double t1 = swap ? PI / 2 - a : a;
       long double t2 = dxneg ? PI - t1 : t1;
       long double t3 = dyneg ? -t2 : t2;
-      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k)] = (double)t3;
+      tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k)] = (double)t3;
       // signed slope: tan(theta) (no swap) or -cot(theta) (swap), exactly +-k / K
       const double sg = (swap ? -1.0 : 1.0) * ((dxneg ^ dyneg) ? -1.0 : 1.0);
-      tab[P2P_TAB_ATAN + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = sg * (double)k / P2P_ATAN_K;
+      tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k) + 1] = sg * (double)k / P2P_ATAN_K;
     }
   }
 }

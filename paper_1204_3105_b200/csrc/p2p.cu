@@ -141,7 +141,7 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
 constexpr int P2P_RS = 32;  // row stride (double2) of the reaction scratch; column c of row lane r sits at c ^ 2r
                             // (conflict-free STS.128 / LDS.128)
 // dynamic shared memory of one block: tables, then per warp sources, strengths, reactions, scratch
-constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1) + 64);
+constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + P2P_ATAN_N);
 constexpr size_t P2P_WARP_BYTES = sizeof(double2) * (2 * P2P_S + 4 * P2P_RS) + sizeof(double) * P2P_S;
 constexpr size_t P2P_SMEM = P2P_TAB_BYTES + P2P_WARPS * P2P_WARP_BYTES;
 constexpr double P2P_PAD = 1.0e30;
@@ -158,7 +158,7 @@ __device__ __forceinline__ PairOut p2p_fast(double dx, double dy, double r2, uin
   double kd, lz;
   p2p_log_split(r2, s_log, &kd, &lz);
   o.lg = fma(kd, P2P_C[12], lz);  // kd ln 2 + lz (one rounding of the exact product sum)
-  o.ag = p2p_atan2(dy, dx, s_atan);
+  o.ag = p2p_atan2<true>(dy, dx, s_atan);
   return o;
 }
 
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     int64_t lo, int64_t hi, DevStatus* st) {
   extern __shared__ double2 smem[];
   double2* s_log = smem;
-  double2* s_atan = s_log + P2P_LOG_N;  // + 64 pad: garbage indices of |z| < 1e-30
+  double2* s_atan = s_log + P2P_LOG_N;  // P2P_ATAN_N entries (garbage k of |z| < 1e-30 stays inside)
   p2p_load_tables(tabs, s_log, s_atan);
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(DIR_T) k_direct(const double2* __restrict__ sx
                                                   int self_mode, const double* __restrict__ tabs,
                                                   double2* __restrict__ phi, unsigned long long* bad) {
   __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1) + 64];
+  __shared__ double2 s_atan[P2P_ATAN_N];
   __shared__ double2 s_x[DIR_T];
   __shared__ double s_u[DIR_T];
   p2p_load_tables(tabs, s_log, s_atan);
@@ -503,13 +503,13 @@ __global__ void __launch_bounds__(DIR_T) k_direct(const double2* __restrict__ sx
 __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
                                  double2* __restrict__ out) {
   __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[8 * (P2P_ATAN_K + 1)];
+  __shared__ double2 s_atan[P2P_ATAN_N];
   p2p_load_tables(tabs, s_log, s_atan);
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double dx = d[i].x, dy = __dadd_rn(d[i].y, 0.0);  // canonical +0 imaginary zero (D13)
   const double r2 = fma(dx, dx, dy * dy);
-  out[i] = make_double2(p2p_log(r2, p2p_smem_addr(s_log)), p2p_atan2(dy, dx, p2p_smem_addr(s_atan)));
+  out[i] = make_double2(p2p_log(r2, p2p_smem_addr(s_log)), p2p_atan2<true>(dy, dx, p2p_smem_addr(s_atan)));
 }
 
 }  // namespace

@@ -25,9 +25,18 @@
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
 #define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
 // table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (theta[oct][k], tau[oct][k]), 8 x (K+1)
+#define P2P_ATAN_SUB 128  // entries per octant sub-table (k = 0..64 used; 65..127 absorb masked garbage)
+#define P2P_ATAN_N (8 * P2P_ATAN_SUB)
 #define P2P_TAB_LOG 0
 #define P2P_TAB_ATAN (2 * P2P_LOG_N)
-#define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * 8 * (P2P_ATAN_K + 1))
+#define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * P2P_ATAN_N)
+
+// atan table entry of (octant, k), octant bit 0 = swap, bit 1 = dx < 0, bit 2 = dy < 0:
+// k + 128 [dx < 0] + 256 [dy < 0] + 512 [swap], so that the pair kernel forms the index from
+// the sign bytes of dx, dy with one PRMT (p2p_atan2<true>)
+__host__ __device__ inline int p2p_atan_index(int oct, int k) {
+  return k + P2P_ATAN_SUB * ((oct >> 1) & 1) + 2 * P2P_ATAN_SUB * ((oct >> 2) & 1) + 4 * P2P_ATAN_SUB * (oct & 1);
+}
 // |z|^2 below this (hi word of 1e-60) takes the exact slow path
 #define P2P_SLOW_HI 0x3379b604
 // z intervals: bit patterns [OFF + i 2^43, OFF + (i+1) 2^43), OFF = 0x3fe6000000000000 - 2^42,
@@ -44,10 +53,21 @@ __constant__ double P2P_C[13] = {
 };
 
 // copy the tables to shared memory (whole block; ends with __syncthreads)
+// s_log[P2P_LOG_N], s_atan[P2P_ATAN_N] (the layout of p2p_atan_index)
 __device__ __forceinline__ void p2p_load_tables(const double* __restrict__ tabs, double2* s_log, double2* s_atan) {
   const double2* t2 = (const double2*)tabs;
   for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
-  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATAN / 2 + i];
+  for (int i = threadIdx.x; i < P2P_ATAN_N; i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATAN / 2 + i];
+  __syncthreads();
+}
+
+// compact copy for p2p_atan2<false>: s_atan[8 * (P2P_ATAN_K + 1)], entry oct * 65 + k
+__device__ __forceinline__ void p2p_load_tables_compact(const double* __restrict__ tabs, double2* s_log,
+                                                        double2* s_atan) {
+  const double2* t2 = (const double2*)tabs;
+  for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
+  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x)
+    s_atan[i] = t2[P2P_TAB_ATAN / 2 + p2p_atan_index(i / (P2P_ATAN_K + 1), i % (P2P_ATAN_K + 1))];
   __syncthreads();
 }
 
@@ -104,6 +124,9 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // Arg(dx + i dy) in (-pi, pi] for |z| >= 1e-30.  dy must not be -0: callers pass a
 // canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
 // so y - x never yields -0 there).
+// SPARSE: atab holds P2P_ATAN_N entries in the p2p_atan_index layout (pair kernel, direct
+// sum, debug hook); else the compact 8 x 65 copy (M2L), where k must be <= 64 (|z| normal)
+template <bool SPARSE>
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
   // Rotation by the reference direction theta of (octant, k): with (P, Q) = (dy, dx), or
   // (-dx, dy) when |dy| > |dx|, and the table's signed slope tau (+-k/64; its sign folds the
@@ -113,11 +136,20 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   const double P = swap ? -dx : dy, Q = swap ? dy : dx;
   double r0;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(Q));
-  const int k = __double2loint(fma(fabs(P * r0), (double)P2P_ATAN_K, 6755399441055744.0)) & 0x7f;  // 0..64
-  // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
+  const int k = __double2loint(fma(fabs(P * r0), (double)P2P_ATAN_K, 6755399441055744.0));  // 0..64 (masked below)
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
-  const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
-  const double2 Tt = p2p_lds2(atab + 16 * (oct * (P2P_ATAN_K + 1) + k));  // (theta[oct][k], tau[oct][k])
+  uint32_t idx;
+  if (SPARSE) {
+    // byte 0 = sign of dx replicated (bit 7 -> +128), byte 1 = sign of dy (bit 8 -> +256)
+    uint32_t sg;
+    asm("prmt.b32 %0, %1, %2, 0xFB;" : "=r"(sg) : "r"(hx), "r"(hy));
+    idx = ((uint32_t)k & 0x7fu) | (sg & 0x180u) | (swap ? 4u * P2P_ATAN_SUB : 0u);
+  } else {
+    // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
+    const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
+    idx = oct * (P2P_ATAN_K + 1) + (k & 0x7f);
+  }
+  const double2 Tt = p2p_lds2(atab + 16 * idx);  // (theta[oct][k], tau[oct][k])
   const double a = fma(-Tt.y, Q, P);
   const double b = fma(Tt.y, P, Q);
   // q = a / b: q0 = a r0 beside the residual e = 1 - b r0, then q0 (1 + e + e^2)

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   double2* s_b = s_lg + NB;              // [32]      L2L part
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
-  p2p_load_tables(tabs, s_log, s_atan);  // ends with __syncthreads
+  p2p_load_tables_compact(tabs, s_log, s_atan);  // ends with __syncthreads
   // A fragments: Cb[r][k] = C(r+k-1, k-1), row r = 8 mt + ln/4, column k = 4 kt + ln%4 + 1
   for (int i = threadIdx.x; i < MT * KT * 32; i += blockDim.x) {
     const int ln = i & 31, kt = (i >> 5) % KT, mt = (i >> 5) / KT;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
         }
         if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
           const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
-          s_lg[s] = make_double2(0.5 * p2p_log(fma(dx, dx, dy * dy), a_log), p2p_atan2(dy, dx, a_atan));
+          s_lg[s] = make_double2(0.5 * p2p_log(fma(dx, dx, dy * dy), a_log), p2p_atan2<false>(dy, dx, a_atan));
           s_q[s] = av[0].x;
         }
       }
