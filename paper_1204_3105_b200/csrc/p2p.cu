@@ -246,6 +246,9 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
       // self mode: the row targets are also sources (their strengths weight the reactions)
       const double u0 = (sym && v0) ? su[tb + row0] : 0.0, u1 = (sym && v1) ? su[tb + row1] : 0.0;
       double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+      // distinct targets only: in the symmetric self-mode kernel the extra path costs the main
+      // loop more (register allocation) than the empty rows it saves
+      const bool last4 = !SELF && tk.w - rc <= 4;
       for (int c0 = sd ? (rc & ~31) : 0; c0 < ns; c0 += 32) {
         if (!whole) {
           if (c0 + lane < ns) {
@@ -260,6 +263,52 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
         const int cb = whole ? c0 : 0;  // chunk base in shared memory
         const int cnt = min(32, ns - c0);
         unsigned hw = 0;  // halves of the chunk whose reaction partials are in s_rs
+        if (last4) {
+          // a last row step of <= 4 rows: one row (tl) and 4 columns 8 j + ph of the chunk per
+          // lane, so that the empty rows tl + 4 cost nothing
+          double vr[4] = {0.0, 0.0, 0.0, 0.0}, vi[4] = {0.0, 0.0, 0.0, 0.0};
+          auto cols1 = [&](auto njc) {
+            constexpr int NJ = decltype(njc)::value;
+            double uc[NJ], dx[NJ], dy[NJ], r2[NJ];
+            PairOut pr[NJ];
+            bool slow = false;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              const double2 x = s_xy[cb + 8 * j + ph];
+              uc[j] = s_u[cb + 8 * j + ph];
+              dx[j] = y0.x - x.x;
+              dy[j] = y0.y - x.y;
+              r2[j] = fma(dx[j], dx[j], dy[j] * dy[j]);
+              pr[j] = p2p_fast(dx[j], dy[j], r2[j], a_log, a_atan);
+              slow |= __double2hiint(r2[j]) < P2P_SLOW_HI;
+            }
+            if (__builtin_expect(slow, 0)) {
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                const int col = c0 + 8 * j + ph;
+                if (__double2hiint(r2[j]) < P2P_SLOW_HI)
+                  pr[j] = p2p_slow(dx[j], dy[j], r2[j], false, tperm, tb + row0, sym ? sb + col : -1, st);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              a0r = fma(uc[j], pr[j].lg, a0r);
+              a0i = fma(uc[j], pr[j].ag, a0i);
+              const double g = pr[j].ag;
+              vr[j] = u0 * pr[j].lg;
+              vi[j] = u0 * (g > 0.0 ? g - PI : g + PI);
+            }
+          };
+          if (cnt > 16)
+            cols1(std::integral_constant<int, 4>{});
+          else
+            cols1(std::integral_constant<int, 2>{});
+          if (sym) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s_rs[tl * P2P_RS + ((8 * j + ph) ^ (2 * tl))] = make_double2(vr[j], vi[j]);
+            hw = cnt > 16 ? 3u : 1u;
+          }
+        } else
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && cnt <= 16) break;  // a short last chunk skips its empty second half
