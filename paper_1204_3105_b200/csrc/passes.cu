@@ -255,7 +255,8 @@ int fmm_stage_upward(fmm_tree_s* t) {
 // M2L in the Pascal-scaled form: for a batch of NB sources s of E4(t),
 //   Y[l][s] = sum_{k=1..p} C(l+k-1, k-1) a~_{s,k},   a~_{s,k} = (-1)^k a_{s,k} w_s^k,
 //   b_l += w_s^l (Y[l][s] - Q_s / l)   (l >= 1),     b_0 += Q_s Log(c_t - c_s) + Y[0][s]
-// The contraction Y = Cb * A~ (Cb: (p+1) x p real; A~: p x 2 NB, real and imaginary parts as
+// The contraction Y = Cb * A~ (Cb: (p+1) x p real, stored as (-1)^k C(l+k-1, k-1) so that the
+// staged A~ is a_{s,k} w_s^k without the sign; A~: p x 2 NB, real and imaginary parts as
 // columns) runs on DMMA (mma.sync m8n8k4 f64, IEEE FP64 multiply-adds): Cb lives in the A
 // fragments of the warp's registers, A~ is staged in shared memory.  Fragment layouts
 // (m8n8k4 .f64): A[r][c] at lane 4r + c; B[k][n] at lane 4n + k; C[r][2c + {0,1}] at lane 4r + c.
@@ -306,11 +307,13 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
   p2p_load_tables_compact(tabs, s_log, s_atan);  // ends with __syncthreads
-  // A fragments: Cb[r][k] = C(r+k-1, k-1), row r = 8 mt + ln/4, column k = 4 kt + ln%4 + 1
+  // A fragments: Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in), row r = 8 mt + ln/4,
+  // column k = 4 kt + ln%4 + 1
   for (int i = threadIdx.x; i < MT * KT * 32; i += blockDim.x) {
     const int ln = i & 31, kt = (i >> 5) % KT, mt = (i >> 5) / KT;
     const int r = 8 * mt + (ln >> 2), k = 4 * kt + (ln & 3) + 1;
-    s_afr[i] = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
+    const double c = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
+    s_afr[i] = (k & 1) ? -c : c;
   }
   double* s_invr = s_afr + MT * KT * 32;  // [8 MT] 1/r (0 for r = 0)
   for (int i = threadIdx.x; i < 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   for (int b0 = 0; b0 < nsrc; b0 += NB) {
     const int nb = min(NB, nsrc - b0);
     // lane = (source s = lane / 4, residue j = lane % 4) owns exponents k = 4m + j: it loads
-    // a_{s,k} (all its loads first), forms w^k and a~_{s,k} = (-1)^k a_{s,k} w^k directly
+    // a_{s,k} (all its loads first), forms w^k and a_{s,k} w^k (the (-1)^k of a~ is in Cb)
     {
       constexpr int NM = P / 4 + 1;
       const int s = lane >> 2, j = lane & 3;
@@ -375,11 +378,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
         for (int m = 0; m < NM; ++m) {
           const int k = 4 * m + j;
           if (k <= P) s_pw[s * (P + 1) + k] = pw;
-          if (k >= 1 && k <= P) {
-            double2 v = cmul(av[m], pw);
-            if (k & 1) v = make_double2(-v.x, -v.y);
-            s_at[s * P + k - 1] = v;
-          }
+          if (k >= 1 && k <= P) s_at[s * P + k - 1] = cmul(av[m], pw);  // (-1)^k is in Cb
           pw = cmul(pw, w4);
         }
         if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
