@@ -54,6 +54,8 @@ void fmm_host_p2p_tables(double* tab) {
       // signed slope: tan(theta) (no swap) or -cot(theta) (swap), exactly +-k / K
       const double sg = (swap ? -1.0 : 1.0) * ((dxneg ^ dyneg) ? -1.0 : 1.0);
       tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k) + 1] = sg * (double)k / P2P_ATAN_K;
+      tab[P2P_TAB_ATANC + 2 * (oct * (P2P_ATAN_K + 1) + k)] = tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k)];
+      tab[P2P_TAB_ATANC + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k) + 1];
     }
   }
 }

@@ -29,7 +29,8 @@
 #define P2P_ATAN_N (8 * P2P_ATAN_SUB)
 #define P2P_TAB_LOG 0
 #define P2P_TAB_ATAN (2 * P2P_LOG_N)
-#define P2P_TAB_DOUBLES (2 * P2P_LOG_N + 2 * P2P_ATAN_N)
+#define P2P_TAB_ATANC (2 * P2P_LOG_N + 2 * P2P_ATAN_N)  // compact copy: entry oct * 65 + k
+#define P2P_TAB_DOUBLES (P2P_TAB_ATANC + 2 * 8 * (P2P_ATAN_K + 1))
 
 // atan table entry of (octant, k), octant bit 0 = swap, bit 1 = dx < 0, bit 2 = dy < 0:
 // k + 128 [dx < 0] + 256 [dy < 0] + 512 [swap], so that the pair kernel forms the index from
@@ -66,8 +67,7 @@ __device__ __forceinline__ void p2p_load_tables_compact(const double* __restrict
                                                         double2* s_atan) {
   const double2* t2 = (const double2*)tabs;
   for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
-  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x)
-    s_atan[i] = t2[P2P_TAB_ATAN / 2 + p2p_atan_index(i / (P2P_ATAN_K + 1), i % (P2P_ATAN_K + 1))];
+  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATANC / 2 + i];
   __syncthreads();
 }
 
