@@ -84,33 +84,37 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 }
 
 // ------------------------------------------------------------------ M2M (one warp per parent, lane = coefficient)
+// a child's multipole is staged once in shared memory (one coalesced load), so that the
+// Horner loop of lane k reads a_j without a memory round trip per step
 __global__ void __launch_bounds__(128) k_m2m(int B, int64_t nparents, int64_t span_l, const int32_t* __restrict__ soff,
                                              const double2* __restrict__ cen_par, const double2* __restrict__ cen_ch,
                                              const double2* __restrict__ mp_ch, int p, const double* __restrict__ binom,
                                              double2* __restrict__ mp_par) {
-  int64_t P = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
+  __shared__ double2 s_a[4][32];
+  const int64_t P = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (P >= nparents) return;
-  double2 cp = cen_par[P];
-  for (int k = lane; k <= p; k += 32) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int ch = 0; ch < B; ++ch) {
-      int64_t c = P * B + ch;
-      if (soff[(c + 1) * span_l] == soff[c * span_l]) continue;
-      const double2* a = mp_ch + c * (p + 1);
-      double Q = a[0].x;
-      if (k == 0) {
-        acc.x += Q;
-        continue;
-      }
-      double2 cc = cen_ch[c];
-      double2 z0 = make_double2(cc.x - cp.x, cc.y - cp.y);
+  const double2 cp = cen_par[P];
+  const int k = lane;  // p <= 31: one coefficient per lane
+  double2 acc = make_double2(0.0, 0.0);
+  for (int ch = 0; ch < B; ++ch) {
+    const int64_t c = P * B + ch;
+    if (soff[(c + 1) * span_l] == soff[c * span_l]) continue;
+    __syncwarp();
+    s_a[w][lane] = lane <= p ? mp_ch[c * (p + 1) + lane] : make_double2(0.0, 0.0);
+    __syncwarp();
+    const double Q = s_a[w][0].x;
+    if (k == 0) {
+      acc.x += Q;
+    } else if (k <= p) {
+      const double2 cc = cen_ch[c];
+      const double2 z0 = make_double2(cc.x - cp.x, cc.y - cp.y);
       double2 h = make_double2(-Q / k, 0.0);
-      for (int j = 1; j <= k; ++j) h = cadd(cmul(h, z0), cscale(binom[(k - 1) * BS + (j - 1)], a[j]));
+      for (int j = 1; j <= k; ++j) h = cadd(cmul(h, z0), cscale(binom[(k - 1) * BS + (j - 1)], s_a[w][j]));
       acc = cadd(acc, h);
     }
-    mp_par[P * (p + 1) + k] = acc;
   }
+  if (k <= p) mp_par[P * (p + 1) + k] = acc;
 }
 
 // ------------------------------------------------------------------ downward v2 (templated on P >= p)
