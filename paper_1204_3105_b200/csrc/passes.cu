@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
       const double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
       s_b[lane] = lane <= p ? loc_par[par * (p + 1) + lane] : make_double2(0.0, 0.0);
       __syncwarp();
-      for (int k = p; k >= 0; --k) {
+#pragma unroll
+      for (int k = P; k >= 0; --k) {  // unrolled: the binomial loads leave the Horner chain
+        if (k > p) continue;
         const double2 bk = s_b[k];
         if (k >= lane && lane <= p) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + lane], bk));
       }
