@@ -459,6 +459,7 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
                                                     const int32_t* __restrict__ tperm,
                                                     const double2* __restrict__ part, int nslot,
                                                     double2* __restrict__ phi) {
+  __shared__ double2 s_loc[4][32];
   const int64_t t = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= hi) return;
@@ -466,7 +467,11 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
   if (nt == 0) return;
   const int nn = nnear[t];
   const double2 c = cen_leaf[t];
-  const double2* b = loc_leaf + t * (p + 1);
+  // the leaf's local expansion in shared memory (one coalesced load), so that the Horner
+  // steps below do not wait on a global load each
+  double2* const b = s_loc[threadIdx.x >> 5];
+  b[lane] = lane <= p ? loc_leaf[t * (p + 1) + lane] : make_double2(0.0, 0.0);
+  __syncwarp();
   for (int i = lane; i < nt; i += 32) {
     const int tpos = tb + i;
     double2 v[NS];
