@@ -50,9 +50,14 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
   double Sr[P + 1], Si[P + 1];
 #pragma unroll
   for (int k = 0; k <= P; ++k) Sr[k] = Si[k] = 0.0;
+  // the next source of the lane is loaded before the current one's power chain (software
+  // pipelining: the load latency overlaps the chain)
+  double2 x = s0 + sub < s1 ? sxy[s0 + sub] : c;
+  double u = s0 + sub < s1 ? su[s0 + sub] : 0.0;
   for (int i = s0 + sub; i < s1; i += 8) {
-    double2 x = sxy[i];
-    double u = su[i];
+    const bool more = i + 8 < s1;
+    const double2 xn = more ? sxy[i + 8] : c;
+    const double un = more ? su[i + 8] : 0.0;
     double zr = x.x - c.x, zi = x.y - c.y;
     double pr = u, pi = 0.0;  // u z^k
     Sr[0] += u;
@@ -64,6 +69,8 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
       Sr[k] += pr;
       Si[k] += pi;
     }
+    x = xn;
+    u = un;
   }
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
