@@ -27,10 +27,9 @@ namespace {
 
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
-// and report the minimal offending index; histogram of keys (K+1 bins) for the CSR.
+// and report the minimal offending index.  (The leaf CSR comes from the sorted keys.)
 __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
-                                              int64_t index_base, uint32_t* __restrict__ key,
-                                              int32_t* __restrict__ hist, DevStatus* st) {
+                                              int64_t index_base, uint32_t* __restrict__ key, DevStatus* st) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 p = xy[i];
@@ -40,10 +39,18 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
     atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
   }
   key[i] = k;
-  // warp-aggregated histogram increment
-  unsigned peers = __match_any_sync(__activemask(), k);
-  int leader = __ffs(peers) - 1;
-  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[k], __popc(peers));
+}
+
+// leaf CSR from the sorted keys: off[k] = #points with key < k, k = 0..K+1; position i
+// (0..n) writes off[k] = i for prev < k <= cur, prev = sorted[i-1] (-1 at i = 0) and
+// cur = sorted[i] (K+1 at i = n), so every entry is written exactly once
+__global__ void __launch_bounds__(256) k_offsets(const uint32_t* __restrict__ sorted, int64_t n, int64_t K,
+                                                 int32_t* __restrict__ off) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int64_t prev = i > 0 ? (int64_t)sorted[i - 1] : -1;
+  const int64_t cur = i < n ? (int64_t)sorted[i] : K + 1;
+  for (int64_t k = prev + 1; k <= cur; ++k) off[k] = (int32_t)i;
 }
 
 // ------------------------------------------------------------------ scan (exclusive, int32)
@@ -378,8 +385,12 @@ static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
 }
 
 // sort (key, iota) pairs stably; writes the permutation (sorted position -> input index)
-static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm) {
-  if (n == 0) return FMM_OK;
+// and the leaf CSR off[0..K+1] from the sorted keys
+static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm, int32_t* off) {
+  if (n == 0) {
+    FMM_CUDA_TRY(cudaMemsetAsync(off, 0, sizeof(int32_t) * (t->g.K + 2), t->stream));
+    return FMM_OK;
+  }
   cudaStream_t s = t->stream;
   const int bits = key_bits(t->g.K);
   const int passes = (bits + RS_MAXB - 1) / RS_MAXB;
@@ -423,6 +434,9 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
     vin = vout;
     shift += db;
   }
+  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
 
@@ -430,31 +444,18 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
-  int64_t K = G.K;
-  // histograms (K+1 bins incl. sentinel), zeroed
-  FMM_CUDA_TRY(cudaMemsetAsync(t->soff, 0, sizeof(int32_t) * (K + 2), s));
-  if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->toff, 0, sizeof(int32_t) * (K + 2), s));
   if (t->n > 0) {
-    k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->soff,
-                                                  t->status);
+    k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->status);
     t->launches++;
   }
   if (!G.self_mode && t->m > 0) {
-    k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->toff,
-                                                  t->status);
+    k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->status);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
-  // exclusive scans of the histograms -> leaf CSR (soff[K] = #in-domain points)
-  size_t sb = fmm_scan_scratch_bytes(K + 2);
-  void* scr = nullptr;
-  FMM_CUDA_TRY(cudaMallocAsync(&scr, sb, s));
-  int e = fmm_device_scan_i32(t->soff, t->soff, K + 2, scr, sb, s, &t->launches);
-  if (!e && !G.self_mode) e = fmm_device_scan_i32(t->toff, t->toff, K + 2, scr, sb, s, &t->launches);
-  cudaFreeAsync(scr, s);
-  if (e) return e;
-  e = radix_sort_perm(t, t->skey, t->n, t->sperm);
-  if (!e && !G.self_mode) e = radix_sort_perm(t, t->tkey, t->m, t->tperm);
+  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain points)
+  int e = radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
+  if (!e && !G.self_mode) e = radix_sort_perm(t, t->tkey, t->m, t->tperm, t->toff);
   if (e) return e;
   if (t->n > 0) {
     k_gather_src<<<blocks_for(t->n, 256), 256, 0, s>>>(t->sperm, t->n, (const double2*)t->src_xy_in, t->src_u_in,
