@@ -28,11 +28,19 @@ namespace {
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
 // and report the minimal offending index.  (The leaf CSR comes from the sorted keys.)
+// With u != nullptr it also packs (x, y, u) into one 32-byte record per point (input
+// order), so that the gather after the sort reads one DRAM sector per point, not two.
 __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
-                                              int64_t index_base, uint32_t* __restrict__ key, DevStatus* st) {
+                                              int64_t index_base, uint32_t* __restrict__ key, DevStatus* st,
+                                              const double* __restrict__ u = nullptr,
+                                              double2* __restrict__ rec = nullptr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 p = xy[i];
+  if (u) {
+    rec[2 * i] = p;
+    rec[2 * i + 1] = make_double2(u[i], 0.0);
+  }
   uint32_t k;
   if (!geo_key(g, p.x, p.y, &k)) {
     k = (uint32_t)g.K;
@@ -227,14 +235,14 @@ __global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __rest
 }
 
 // ------------------------------------------------------------------ gathers
-__global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
-                             const double* __restrict__ u, double2* __restrict__ sxy, double* __restrict__ su) {
+__global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ rec,
+                             double2* __restrict__ sxy, double* __restrict__ su) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int32_t j = perm[i];
-  const double2 v = xy[j];
+  const int64_t j = perm[i];
+  const double2 v = rec[2 * j], w = rec[2 * j + 1];  // one 32-byte sector
   sxy[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
-  su[i] = u[j];
+  su[i] = w.x;
 }
 __global__ void k_gather_xy(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
                             double2* __restrict__ out) {
@@ -444,8 +452,11 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
+  double2* rec = nullptr;  // (x, y, u, 0) per source, input order
   if (t->n > 0) {
-    k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->status);
+    FMM_CUDA_TRY(cudaMallocAsync((void**)&rec, (size_t)t->n * 32, s));
+    k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->status,
+                                                  t->src_u_in, rec);
     t->launches++;
   }
   if (!G.self_mode && t->m > 0) {
@@ -456,11 +467,14 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain points)
   int e = radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
   if (!e && !G.self_mode) e = radix_sort_perm(t, t->tkey, t->m, t->tperm, t->toff);
-  if (e) return e;
+  if (e) {
+    if (rec) cudaFreeAsync(rec, s);
+    return e;
+  }
   if (t->n > 0) {
-    k_gather_src<<<blocks_for(t->n, 256), 256, 0, s>>>(t->sperm, t->n, (const double2*)t->src_xy_in, t->src_u_in,
-                                                        t->sxy, t->su);
+    k_gather_src<<<blocks_for(t->n, 256), 256, 0, s>>>(t->sperm, t->n, rec, t->sxy, t->su);
     t->launches++;
+    cudaFreeAsync(rec, s);
   }
   if (!G.self_mode && t->m > 0) {
     k_gather_xy<<<blocks_for(t->m, 256), 256, 0, s>>>(t->tperm, t->m, (const double2*)t->tgt_xy_in, t->txy);
