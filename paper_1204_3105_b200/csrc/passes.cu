@@ -35,15 +35,19 @@ __device__ __forceinline__ double2 clog_principal(double dx, double dy) {
   return make_double2(0.5 * log(dx * dx + dy * dy), atan2(dy, dx));
 }
 
-// ------------------------------------------------------------------ P2M (one warp per leaf)
-// 8 lanes per leaf (4 leaves per warp): each lane accumulates u z^k over every 8th source of
-// its leaf, then a 3-step xor reduction within the 8-lane group.
+// ------------------------------------------------------------------ P2M (lane groups per leaf)
+// P2M_LPL lanes per leaf (4: 8 leaves per warp; 8 and 16 were slower, 2 slower on the
+// clustered C5): each lane accumulates u z^k over every P2M_LPL-th source of its leaf, then
+// an xor reduction within the lane group.
+#ifndef P2M_LPL
+#define P2M_LPL 4
+#endif
 template <int P>
 __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, const double* __restrict__ su,
                                              const int32_t* __restrict__ soff, const double2* __restrict__ cen,
                                              int64_t K, int p, double2* __restrict__ mp) {
-  const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
-  const int sub = threadIdx.x & 7;
+  const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / P2M_LPL;
+  const int sub = threadIdx.x & (P2M_LPL - 1);
   const bool lvalid = leaf < K;
   const int s0 = lvalid ? soff[leaf] : 0, s1 = lvalid ? soff[leaf + 1] : 0;
   const double2 c = lvalid ? cen[leaf] : make_double2(0.0, 0.0);
@@ -54,10 +58,10 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
   // pipelining: the load latency overlaps the chain)
   double2 x = s0 + sub < s1 ? sxy[s0 + sub] : c;
   double u = s0 + sub < s1 ? su[s0 + sub] : 0.0;
-  for (int i = s0 + sub; i < s1; i += 8) {
-    const bool more = i + 8 < s1;
-    const double2 xn = more ? sxy[i + 8] : c;
-    const double un = more ? su[i + 8] : 0.0;
+  for (int i = s0 + sub; i < s1; i += P2M_LPL) {
+    const bool more = i + P2M_LPL < s1;
+    const double2 xn = more ? sxy[i + P2M_LPL] : c;
+    const double un = more ? su[i + P2M_LPL] : 0.0;
     double zr = x.x - c.x, zi = x.y - c.y;
     double pr = u, pi = 0.0;  // u z^k
     Sr[0] += u;
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
+    for (int o = 1; o < P2M_LPL; o <<= 1) {
       Sr[k] += __shfl_xor_sync(0xffffffffu, Sr[k], o);
       Si[k] += __shfl_xor_sync(0xffffffffu, Si[k], o);
     }
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
   double2* out = mp + leaf * (p + 1);
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
-    if (k <= p && sub == (k & 7)) {
+    if (k <= p && sub == (k & (P2M_LPL - 1))) {
       out[k] = (k == 0) ? make_double2(Sr[0], 0.0) : make_double2(-Sr[k] / k, -Si[k] / k);
     }
   }
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int
 template <int P>
 void launch_p2m(fmm_tree_s* t) {
   const Geo& G = t->g;
-  k_p2m<P><<<(unsigned)((G.K * 8 + 127) / 128), 128, 0, t->stream>>>(
+  k_p2m<P><<<(unsigned)((G.K * P2M_LPL + 127) / 128), 128, 0, t->stream>>>(
       t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], G.K, G.p, t->mp + G.lvl_off[G.L] * (G.p + 1));
 }
 
