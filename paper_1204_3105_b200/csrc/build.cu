@@ -253,10 +253,24 @@ __global__ void k_gather_xy(const int32_t* __restrict__ perm, int64_t n, const d
 }
 
 // ------------------------------------------------------------------ centres (D12)
-__global__ void k_centres(DGeo g, int l, int64_t ncells, double2* __restrict__ out) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncells) return;
-  out[c] = geo_centre(g, l, c);
+// level offsets of the all-level cell arrays (level l = cells [off[l], off[l+1]))
+struct LevelOffsets {
+  int64_t off[18];
+  int nl;  // levels 0..nl-1
+};
+__device__ inline int level_of(const LevelOffsets& lo, int64_t gi) {
+  int l = 0;
+  while (l + 1 < lo.nl && gi >= lo.off[l + 1]) ++l;
+  return l;
+}
+
+// every cell of every level in one launch (the small upper levels would each be a
+// latency-bound launch of their own)
+__global__ void k_centres(DGeo g, LevelOffsets lo, double2* __restrict__ out) {
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gi >= lo.off[lo.nl]) return;
+  const int l = level_of(lo, gi);
+  out[gi] = geo_centre(g, l, gi - lo.off[l]);
 }
 
 // ------------------------------------------------------------------ interaction lists
@@ -278,12 +292,17 @@ __device__ inline void sort_small(int64_t* v, int n) {
 
 // Candidates, one thread per parent P at level l-1: Children(P U Neighbors(P, l-1)) with
 // sources, ascending (none when no child of P has targets of this rank).
-__global__ void k_cand_level(DGeo g, int l, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
-                             int32_t* __restrict__ cand, int32_t* __restrict__ ncand, int64_t leaf_lo,
-                             int64_t leaf_hi) {
-  int64_t P = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t nparents = ipow_d(g.B, l - 1);
-  if (P >= nparents) return;
+// candidates of every parent cell P of levels 0..L-1 (children level l = level(P) + 1), one launch;
+// cand / ncand are the all-level arrays indexed by the parent's global cell index
+__global__ void k_cand_level(DGeo g, LevelOffsets lvo, const int32_t* __restrict__ soff,
+                             const int32_t* __restrict__ toff, int32_t* __restrict__ cand_all,
+                             int32_t* __restrict__ ncand_all, int64_t leaf_lo, int64_t leaf_hi) {
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gi >= lvo.off[g.L]) return;  // parents live on levels 0..L-1
+  const int l = level_of(lvo, gi) + 1;
+  const int64_t P = gi - lvo.off[l - 1];
+  int32_t* const cand = cand_all + lvo.off[l - 1] * FMM_CAND_MAX;
+  int32_t* const ncand = ncand_all + lvo.off[l - 1];
   const int B = g.B;
   int64_t span_l = ipow_d(B, g.L - l), span_p = span_l * B;
   // parent's target range intersected with this rank's leaf range
@@ -313,11 +332,17 @@ __global__ void k_cand_level(DGeo g, int l, const int32_t* __restrict__ soff, co
 
 // E4 masks, one thread per cell t at level l: bit i set iff cand[parent][i] is not in
 // {t} U Neighbors(t, l)  (NeighborsE4, reading D1); 0 when t has no targets.
-__global__ void k_e4mask_level(DGeo g, int l, const int32_t* __restrict__ toff, const int32_t* __restrict__ cand,
-                               const int32_t* __restrict__ ncand, unsigned long long* __restrict__ e4mask,
-                               int64_t leaf_lo, int64_t leaf_hi) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= ipow_d(g.B, l)) return;
+// E4 masks of every cell of levels 1..L in one launch (after k_cand_level)
+__global__ void k_e4mask_level(DGeo g, LevelOffsets lvo, const int32_t* __restrict__ toff,
+                               const int32_t* __restrict__ cand_all, const int32_t* __restrict__ ncand_all,
+                               unsigned long long* __restrict__ e4mask_all, int64_t leaf_lo, int64_t leaf_hi) {
+  const int64_t gi = lvo.off[1] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gi >= lvo.off[g.L + 1]) return;
+  const int l = level_of(lvo, gi);
+  const int64_t t = gi - lvo.off[l];
+  const int32_t* const cand = cand_all + lvo.off[l - 1] * FMM_CAND_MAX;
+  const int32_t* const ncand = ncand_all + lvo.off[l - 1];
+  unsigned long long* const e4mask = e4mask_all + lvo.off[l];
   int64_t span_l = ipow_d(g.B, g.L - l);
   int64_t tl = t * span_l, th = tl + span_l;
   bool t_has = (th > leaf_lo && tl < leaf_hi) && (toff[min(th, leaf_hi)] - toff[max(tl, leaf_lo)] > 0);
@@ -545,21 +570,18 @@ int fmm_stage_tables_lists(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
-  for (int l = 0; l <= G.L; ++l) {
-    k_centres<<<blocks_for(G.ncells[l], 256), 256, 0, s>>>(g, l, G.ncells[l], t->centre + G.lvl_off[l]);
-    t->launches++;
-  }
+  LevelOffsets lvo;
+  lvo.nl = G.L + 1;
+  for (int l = 0; l <= G.L + 1; ++l) lvo.off[l] = G.lvl_off[l];
+  k_centres<<<blocks_for(G.lvl_off[G.L + 1], 256), 256, 0, s>>>(g, lvo, t->centre);
+  t->launches++;
   int e = fmm_stage_near_partition(t);
   if (e) return e;
-  for (int l = 1; l <= G.L; ++l) {
-    int64_t np = G.ncells[l - 1];
-    k_cand_level<<<blocks_for(np, 128), 128, 0, s>>>(g, l, t->soff, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
-                                                     t->ncand + G.lvl_off[l - 1], t->leaf_lo, t->leaf_hi);
-    k_e4mask_level<<<blocks_for(G.ncells[l], 128), 128, 0, s>>>(g, l, t->toff, t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
-                                                                t->ncand + G.lvl_off[l - 1], t->e4mask + G.lvl_off[l],
+  k_cand_level<<<blocks_for(G.lvl_off[G.L], 128), 128, 0, s>>>(g, lvo, t->soff, t->toff, t->cand, t->ncand,
                                                                 t->leaf_lo, t->leaf_hi);
-    t->launches += 2;
-  }
+  k_e4mask_level<<<blocks_for(G.lvl_off[G.L + 1] - G.lvl_off[1], 128), 128, 0, s>>>(
+      g, lvo, t->toff, t->cand, t->ncand, t->e4mask, t->leaf_lo, t->leaf_hi);
+  t->launches += 2;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
