@@ -160,15 +160,18 @@ def run_gpu(args):
         outs[nm] = torch.zeros(w.m, dtype=torch.complex128, device=dev)
         host_out[nm] = [torch.zeros(w.m, dtype=torch.complex128).pin_memory() for _ in range(2)]
 
-    # e2e: two CUDA streams per tiling, alternating by step (double buffering), so that the
-    # host<->device copies of one step overlap the kernels of the previous step and of the other
-    # tilings; all streams join before the end event.  The device-resident timed region keeps
-    # one stream, so that each kernel's event time is its own (roofline).
+    # e2e leg (the headline's end-to-end number): the same steps through the C ABI with pinned
+    # HOST buffers, serial on the one timed stream like the device-resident value: every step
+    # copies its inputs host -> device inside fmm_build_tree and Phi device -> host inside
+    # fmm_evaluate.  The optional pipelined variant (--e2e-pipelined) alternates two streams
+    # per tiling so that copies overlap kernels of other steps; it is reported separately.
     side = [{nm: torch.cuda.Stream(dev) for nm in names} for _ in range(2)]
 
-    def one_step(timing=False, host=False, fork=True, join=True, parity=0):
-        launches, stage = 0, {}
-        streams = side[parity] if (host and not args.serial) else {nm: stream for nm in names}
+    def one_step(timing=False, host=False, pipelined=False, fork=True, join=True, parity=0, kept=None):
+        """one build + evaluate per tiling; every tree releases its device memory stream-ordered
+        at the end of its own evaluation, so one tree's memory is live at a time"""
+        launches = 0
+        streams = side[parity] if pipelined else {nm: stream for nm in names}
         for nm in names:
             if fork and streams[nm] is not stream:
                 streams[nm].wait_stream(stream)
@@ -178,45 +181,41 @@ def run_gpu(args):
             t = fmm.Tree(cfg_of(w, timing), src, u, tgt, stream=st)
             t.evaluate(host_out[nm][parity] if host else outs[nm], stream=st)
             launches += t.launch_count()
-            if timing:
-                stage[nm] = t
+            if kept is not None:
+                t.release()  # stream-ordered; the handle keeps its stage events
+                kept.append((nm, t))
             else:
                 t.close()
         for nm in names:
             if join and streams[nm] is not stream:
                 stream.wait_stream(streams[nm])
-        return launches, stage
+        return launches
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # warm-up (also checks device status once)
+    # warm-up, then one checked tree per tiling (device status, counters, slab size)
     for i in range(args.warmup):
         one_step()
     barrier()
-    # correctness guard: status of one tree
-    tree_bytes = {}
+    counters, tree_bytes = {}, {}
     for nm, (w, d) in inputs.items():
         src, u, tgt = dev_in[nm]
         t = fmm.Tree(cfg_of(w), src, u, tgt, stream=stream)
         t.evaluate(outs[nm], stream=stream)
         t.check()
-        cnt = counters_for(t)
-        inputs[nm] = (w, d, cnt)
+        counters[nm] = counters_for(t)
         tree_bytes[nm] = t.nbytes()
         t.close()
-    # the timed loop keeps its trees alive until the end (no host syncs inside it): grow the
-    # stream-ordered pool up front so that no timed step pays for first-touch allocation
+    # trees are released stream-ordered as each finishes, so one tree (plus its build scratch)
+    # is live at a time whatever --steps is: grow the pool once to that size, so that no timed
+    # step pays for first-touch allocation (the warm-up steps have usually done so already)
     torch.cuda.synchronize(dev)
-    fmm.native.pool_reserve(int(1.05 * args.steps * sum(tree_bytes.values())) + (1 << 30))
-    inputs2 = {nm: v[:2] for nm, v in inputs.items()}
-    counters = {nm: v[2] for nm, v in inputs.items()}
-    inputs.clear()
-    inputs.update(inputs2)
+    fmm.native.pool_reserve(int(1.5 * max(tree_bytes.values())) + (1 << 30))
 
-    # ---- timed region: device-resident inputs
+    # ---- timed region: device-resident inputs, one stream
     clocks = Clocks()
     clocks.start()
     barrier()
@@ -224,31 +223,27 @@ def run_gpu(args):
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
     launches = 0
-    p2p_ms, down_ms, up_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
-    build_ms, pair_ms = {nm: 0.0 for nm in names}, {nm: 0.0 for nm in names}
-    kept = []  # trees stay alive until after the timed region (no host syncs inside it)
-    for s in range(args.steps):
-        step_ev[s].record(stream)
-        n_l, trees = one_step(timing=True)
-        launches += n_l
-        kept.append(trees)
+    kept = []  # released handles: their stage events are read after the timed region
+    for s_ in range(args.steps):
+        step_ev[s_].record(stream)
+        launches += one_step(timing=True, kept=kept)
     step_ev[args.steps].record(stream)
     e1.record(stream)
     barrier()
+    clk = clocks.stop(local)
     ms_total = e0.elapsed_time(e1)
     step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     log(f"[bench] per-step ms: {[round(x, 2) for x in step_ms]}")
-    for trees in kept:
-        for nm, t in trees.items():
-            ms = t.stage_times()
-            build_ms[nm] += ms[0] + ms[1]
-            pair_ms[nm] += ms[2]
-            up_ms[nm] += ms[3]
-            down_ms[nm] += ms[4]
-            p2p_ms[nm] += ms[5]
-            t.close()
+    build_ms, pair_ms, up_ms, down_ms, p2p_ms = ({nm: 0.0 for nm in names} for _ in range(5))
+    for nm, t in kept:
+        ms = t.stage_times()
+        build_ms[nm] += ms[0] + ms[1]
+        pair_ms[nm] += ms[2]
+        up_ms[nm] += ms[3]
+        down_ms[nm] += ms[4]
+        p2p_ms[nm] += ms[5]
+        t.close()
     kept.clear()
-    clk = clocks.stop(local)
     ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -256,23 +251,25 @@ def run_gpu(args):
     total_targets = sum(inputs[nm][0].m for nm in names) * args.steps
 
     # ---- e2e: same metric through the C ABI with pinned host buffers (H2D + D2H inside)
-    for i in range(1):
-        one_step(host=True)
-    barrier()
-    t0 = time.perf_counter()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    # consecutive steps pipeline: a tiling's next H2D copy waits only for its own previous
-    # step (its stream), not for the other tilings; all streams join before the end event
-    for s in range(args.steps):
-        one_step(host=True, fork=(s < 2), join=(s >= args.steps - 2), parity=s % 2)
-    f1.record(stream)
-    barrier()
-    e2e_ms = f0.elapsed_time(f1)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_t.item())
+    def e2e_run(pipelined):
+        one_step(host=True, pipelined=pipelined)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for s_ in range(args.steps):
+            if pipelined:  # a tiling's next copy waits only for its own previous step
+                one_step(host=True, pipelined=True, fork=(s_ < 2), join=(s_ >= args.steps - 2), parity=s_ % 2)
+            else:
+                one_step(host=True)
+        f1.record(stream)
+        barrier()
+        t_ = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
+
+    e2e_ms = e2e_run(False)
+    e2e_pipe_ms = e2e_run(True) if args.e2e_pipelined else None
     h2d = sum(w.n * 24 + (0 if w.self_mode else w.m * 16) for w, _ in inputs.values())
     d2h = sum(w.m * 16 for w, _ in inputs.values())
 
@@ -320,15 +317,22 @@ def run_gpu(args):
         "data": "synthetic, seeded numpy PCG64 (fmm_inputs), shapes of BASELINE.json configs",
         "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
                    "tilings": names, "step": "fmm_build_tree + fmm_evaluate per tiling",
-                   "streams": "timed region: one stream; e2e: " + ("one stream" if args.serial else "two CUDA streams per tiling alternating by step (copies overlap kernels), joined at the end"),
+                   "streams": "timed region and e2e: one stream, steps serial",
+                   "memory": "each tree is released stream-ordered after its evaluation (one tree live at a time)",
                    "l2": "inputs larger than L2 (>= 400 MB per tiling)", "per_tiling": per_tiling},
         "roofline": roof,
         "roofline_m2l": roof_m2l,
         "e2e": {"value": total_targets / (e2e_ms / 1e3), "unit": "target evals/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+                "how": "fmm_build_tree from pinned host inputs + fmm_evaluate into a pinned host output, "
+                       "serial on the timed stream (copies inside the timed region)"},
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if e2e_pipe_ms is not None:
+        res["e2e_pipelined"] = {"value": total_targets / (e2e_pipe_ms / 1e3), "unit": "target evals/s",
+                                "how": "two CUDA streams per tiling alternating by step: a step's copies overlap "
+                                       "other steps' kernels (not comparable with the serial device-timed value)"}
     if not args.no_cpu_baseline and world == 1:
         res["cpu_baseline"] = cpu_baseline(args, names, sample_targets=args.cpu_sample)
     if world > 1:
@@ -356,55 +360,87 @@ def oracle_time(w, d, sample_targets, seed=0):
     return est, t2 - t0, len(ids)
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(args, names, sample_targets):
+    """the oracle as it stands on the box's host cores: at all cores (the reported value) and
+    at one thread, each on a bounded sample (oracle_time)"""
     import oracle
 
     inputs = {nm: (fi.get(nm), fi.generate(fi.get(nm))) for nm in names}
-    est, spent, ns = 0.0, 0.0, 0
-    for nm, (w, d) in inputs.items():
-        e, s, k = oracle_time(w, d, sample_targets)
-        est += e
-        spent += s
-        ns += k
     total = sum(w.m for w, _ in inputs.values())
-    return {"value": total / est, "unit": "target evals/s", "cores": oracle.num_threads(), "kind": "oracle",
+    res = {}
+    for label, threads, samp in (("all", os.cpu_count() or 1, sample_targets), ("one", 1, max(64, sample_targets // 4))):
+        oracle.set_num_threads(threads)
+        est, spent = 0.0, 0.0
+        for nm, (w, d) in inputs.items():
+            e, s_, _ = oracle_time(w, d, samp)
+            est += e
+            spent += s_
+        res[label] = (total / est, oracle.num_threads(), samp, spent)
+    oracle.set_num_threads(os.cpu_count() or 1)
+    v, cores, samp, spent = res["all"]
+    v1, _, samp1, spent1 = res["one"]
+    return {"value": v, "unit": "target evals/s", "cores": cores, "kind": "oracle",
             "sample": f"full keying+sort+upward pass on every point of {', '.join(names)}, downward+L2P+P2P "
-                      f"for {sample_targets} random targets per tiling, extrapolated to all targets; "
-                      f"{spent:.1f} s of CPU wall time"}
+                      f"for {samp} random targets per tiling, extrapolated to all targets; "
+                      f"{spent:.1f} s of CPU wall time",
+            "extrapolated": True,
+            "single_thread": {"value": v1, "unit": "target evals/s", "cores": 1,
+                              "sample": f"same, {samp1} targets per tiling; {spent1:.1f} s of CPU wall time"},
+            "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference(args):
+    """the tier's reference arm: the CPU oracle as it stands on the box's host cores.  A step
+    is the bounded sample of oracle_time per tiling (full build + upward pass, downward + L2P
+    + P2P for --cpu-sample targets); `ms_per_step` is the measured wall time of that sampled
+    step, `value` the throughput extrapolated to every target (`extrapolated`: true)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     import oracle
 
+    oracle.set_num_threads(os.cpu_count() or 1)
     names = WORKLOADS[args.workload]
     inputs = {nm: (fi.get(nm), fi.generate(fi.get(nm))) for nm in names}
-    # each step: a bounded sample of the workload (see oracle_time)
-    for i in range(args.warmup):
-        pass  # the oracle has no warm state worth discarding; warm-up steps are skipped
-    ests, spent = [], 0.0
+    # the oracle has no warm state worth discarding (no JIT, no caches across trees): warm-up
+    # steps are skipped
+    ests, walls = [], []
     for s in range(args.steps):
-        est = 0.0
+        est, wall = 0.0, 0.0
         for nm, (w, d) in inputs.items():
             e, sp, _ = oracle_time(w, d, args.cpu_sample, seed=s)
             est += e
-            spent += sp
+            wall += sp
         ests.append(est)
+        walls.append(wall)
     total = sum(w.m for w, _ in inputs.values())
-    ms = 1e3 * sum(ests) / len(ests)
-    value = total / (ms / 1e3)
+    ms_extrap = 1e3 * sum(ests) / len(ests)
+    value = total / (ms_extrap / 1e3)
     cores = oracle.num_threads()
+    sample = (f"per step: full keying+sort+upward pass over every point, downward+L2P+P2P for {args.cpu_sample} "
+              f"random targets per tiling ({args.cpu_sample * len(names)} targets per step); value extrapolated "
+              f"to all {total} targets; {sum(walls):.1f} s CPU wall time total")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "target evals/s",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "ms_per_step": 1e3 * sum(walls) / len(walls), "ms_per_step_extrapolated": ms_extrap,
+            "extrapolated": True, "sample_targets_per_step": args.cpu_sample * len(names),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic, seeded numpy PCG64 (fmm_inputs)",
             "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
                        "tilings": names},
             "cpu_baseline": {"value": value, "unit": "target evals/s", "cores": cores, "kind": "oracle",
-                             "sample": f"per step: full keying+sort+upward pass, {args.cpu_sample} sampled targets "
-                                       f"per tiling, extrapolated; {spent:.1f} s CPU wall time total"},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "target evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -416,9 +452,23 @@ def main():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--serial", action="store_true", help="e2e on one stream too (no copy/compute overlap)")
+    ap.add_argument("--e2e-pipelined", action="store_true",
+                    help="also report e2e with two streams per tiling (copies overlap other steps' kernels)")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if args.impl == "b200" and args.gpus > 1 and world is None:
+        # --gpus N without a launcher: start N ranks (one process per GPU) on this node
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if args.impl == "b200" and world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     res = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if res is not None:
         print(json.dumps(res), flush=True)

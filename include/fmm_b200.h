@@ -21,6 +21,7 @@
  *   FMM_ECOINCIDENT   3  a target coincides with a source of another index (D16)
  *   FMM_ECUDA         4  CUDA runtime error (message: fmm_error_string / fmm_last_error_message)
  *   FMM_ENOMEM        5  device allocation failed
+ *   FMM_ENCCL         6  NCCL unavailable or an NCCL call failed (message: fmm_last_error_message)
  *   FMM_EEXTENSION    7  the library was built without support for the request
  * Domain and coincidence errors are detected on the device; they are reported
  * by the next synchronising call (fmm_status, fmm_export).
@@ -41,12 +42,27 @@ extern "C" {
 #define FMM_ECOINCIDENT 3
 #define FMM_ECUDA 4
 #define FMM_ENOMEM 5
+#define FMM_ENCCL 6
 #define FMM_EEXTENSION 7
 
 /* tilings: square quadtree (Morton Z), septree, triangle-quadtree */
 #define FMM_QUADTREE 0
 #define FMM_SEPTREE 1
 #define FMM_TRIQUAD 2
+
+/* Multi-GPU communicator: an NCCL communicator owned by this
+ * library (NCCL is loaded at run time from libnccl.so.2; no link-time dependency).  Rank 0
+ * calls fmm_comm_unique_id and sends the FMM_COMM_ID_BYTES bytes to every rank (for example
+ * by a torch.distributed broadcast); every rank then calls fmm_comm_init with its CUDA device
+ * current.  One communicator serves any number of trees on that device, used from one host
+ * thread at a time.  Errors: FMM_EBADCFG (arguments), FMM_ENCCL (NCCL missing or failing). */
+#define FMM_COMM_ID_BYTES 128
+typedef struct fmm_comm_s* fmm_comm_t;
+int fmm_comm_unique_id(void* id);
+int fmm_comm_init(const void* id, int32_t nranks, int32_t rank, fmm_comm_t* out);
+int fmm_comm_destroy(fmm_comm_t comm);
+/* NCCL version code of the loaded libnccl (e.g. 22809), 0 when NCCL cannot be loaded */
+int fmm_nccl_version(void);
 
 /* Configuration.  Frames (D7, D8, D11):
  *   FMM_QUADTREE: root_x, root_y = lower-left corner of the root square; root_size = its side.
@@ -61,10 +77,17 @@ extern "C" {
  *           pads with points at 1e30), root_size > 0, all finite; else FMM_EBADCFG.
  * p       : expansion terms, 1..31 (multipole Q, a_1..a_p; local b_0..b_p).
  * self_mode: 1 when targets are the sources; the pair (i, i) is skipped by index (D16).
- * rank / nranks: target-leaf partition for multi-GPU runs;
- *                single GPU: 0 / 1.  Every rank gets the full input; rank r evaluates
- *                the targets of its work-balanced leaf range (fmm_partition,
- *                fmm_rank_range). */
+ * rank / nranks: target-leaf partition for multi-GPU runs; single GPU: 0 / 1.
+ *                Every rank gets the full input (replicated); it keys every point, cuts the
+ *                leaves into work-balanced contiguous key ranges (fmm_partition; a range is a
+ *                union of subtrees), and then sorts, keeps and evaluates only the
+ *                points of its own leaf range plus the halo of near source leaves.  P2M / M2M
+ *                run over its own source leaves only; the per-level multipole tree is summed
+ *                over the ranks by one ncclAllReduce on `comm` (overlapped with the P2P pair
+ *                kernel), or by the caller between fmm_evaluate_begin and fmm_evaluate_end.
+ *                Rank r writes Phi of the targets in its leaf range only.
+ * comm   : fmm_comm_t of this rank (nranks > 1), or NULL.  With nranks > 1 and comm NULL,
+ *          fmm_evaluate is refused (FMM_EBADCFG); use the begin / end pair instead. */
 typedef struct {
   int32_t tiling;
   int32_t depth;
@@ -77,6 +100,7 @@ typedef struct {
   int32_t nranks;
   int32_t flags;       /* FMM_FLAG_* */
   int32_t reserved[5]; /* must be zero */
+  fmm_comm_t comm;     /* multi-GPU communicator or NULL */
 } fmm_config;
 
 /* flags: record per-stage CUDA events from fmm_build_tree on (see fmm_stage_times) */
@@ -99,8 +123,9 @@ typedef struct fmm_tree_s* fmm_tree_t;
 int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* src_u, int64_t n,
                    const double* tgt_xy, int64_t m, void* stream, fmm_tree_t* out);
 
-/* Evaluate Phi for all m targets of this rank: P2M, M2M (upward), M2L + L2L per
- * level (downward), then the P2P near field and L2P.  phi_out: m complex128
+/* Evaluate Phi for all m targets of this rank: P2M, M2M (upward; multi-GPU: own leaves, then
+ * the multipole all-reduce on a high-priority side stream), the P2P pair kernel, M2L + L2L per
+ * level (downward), then the near-field sums and L2P.  phi_out: m complex128
  * values (interleaved re, im) in the caller's target order; device or host memory
  * (host: copied back on `stream`; the caller synchronises the stream).  Targets
  * owned by other ranks are left untouched.  Repeated evaluations are bitwise
@@ -108,6 +133,20 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
  * with n_t n_s > 65,536 points pairs), whose column sums are added atomically (equal
  * to rounding). */
 int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream);
+
+/* fmm_evaluate in two halves, for a multipole exchange done by the caller (nranks > 1 without
+ * a comm; with a comm the all-reduce is enqueued by begin):
+ *   begin: P2M + M2M over this rank's own source leaves (the partial multipole tree), then the
+ *          P2P pair kernel (which needs no multipoles);
+ *   end  : M2L + L2L over every level (using the multipole tree as it is in memory), the
+ *          near-field sums and L2P into phi_out (as fmm_evaluate).
+ * Between them the caller replaces the multipole tree (fmm_multipole_buffer) by the sum of
+ * every rank's partial tree.  With nranks == 1 begin + end == fmm_evaluate. */
+int fmm_evaluate_begin(fmm_tree_t t, void* stream);
+int fmm_evaluate_end(fmm_tree_t t, double* phi_out, void* stream);
+/* device pointer and byte size of the tree's multipole array: complex128 [cells of levels
+ * 0..L][p+1], level-major (level l starts at cell sum_{k<l} B^k) */
+int fmm_multipole_buffer(fmm_tree_t t, void** dev_ptr, size_t* bytes);
 
 /* Replace the strengths (same geometry) so the tree can be re-evaluated. */
 int fmm_set_strengths(fmm_tree_t t, const double* src_u, void* stream);
@@ -178,6 +217,14 @@ size_t fmm_tree_bytes(fmm_tree_t t);
 int64_t fmm_launch_count(fmm_tree_t t);
 
 void fmm_free(fmm_tree_t t);
+
+/* Return the tree's device buffers to the stream-ordered pool (freed on the tree's stream,
+ * after the work already enqueued on it) while the handle stays valid for fmm_stage_times,
+ * fmm_launch_count, fmm_rank_range and fmm_free.  Every call that needs device data
+ * (fmm_evaluate, fmm_set_strengths, fmm_status, fmm_export) then returns FMM_EBADCFG.
+ * Lets a caller run many build + evaluate steps back to back, reading the per-stage times
+ * afterwards, with the memory of one step live at a time.  Errors: FMM_EBADCFG (NULL). */
+int fmm_release(fmm_tree_t t);
 
 /* Depth selection.  Cost of one build + evaluate at `depth`:
  *   uc == NULL: the paper's appendix model (Table 2),

@@ -92,6 +92,7 @@ def lib():
             "orc_tree_evaluate": (C.c_int, [C.c_void_p, _i64, C.c_int64, _d, _i64, _i64]),
             "orc_tree_bound": (None, [C.c_void_p, _i64, C.c_int64, _d]),
             "orc_num_threads": (C.c_int, []),
+            "orc_set_num_threads": (None, [C.c_int]),
             "orc_paper_cost": (C.c_double, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
             "orc_paper_depth": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]),
             "orc_draw": (C.c_uint64, [C.c_uint64, C.c_uint64]),
@@ -411,6 +412,11 @@ class Tree:
 
 def num_threads():
     return int(lib().orc_num_threads())
+
+
+def set_num_threads(n):
+    """OpenMP thread count of the oracle's parallel loops (results do not depend on it)"""
+    lib().orc_set_num_threads(int(n))
 
 
 def paper_cost(tiling, n, m, p, depth):

@@ -37,6 +37,16 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* thread count of the OpenMP loops (bench.py times the oracle at 1 thread and at all cores;
+ * results are identical at any count) */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 static int branching(int tiling) { return tiling == ORC_SEPT ? 7 : 4; }
 
 static int64_t ipow(int64_t b, int e) {

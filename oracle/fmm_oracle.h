@@ -122,6 +122,7 @@ void orc_tree_bound(orc_tree* t, const int64_t* tgt_ids, int64_t ntgt, double* b
 
 /* version / thread count used by OpenMP loops */
 int orc_num_threads(void);
+void orc_set_num_threads(int n);
 
 /* NEXT-2: the appendix cost model and its depth of least cost (1..maxdepth) */
 double orc_paper_cost(int tiling, double n, double m, int p, int depth);

@@ -6,6 +6,7 @@ CUDA kernels of libfmm_b200.so.  There is no CPU fallback; importing the
 binding without the built library raises.
 """
 from .native import (  # noqa: F401
+    Comm,
     Config,
     FmmError,
     Tree,
@@ -18,8 +19,9 @@ from .native import (  # noqa: F401
     UnitCosts,
     choose_depth,
     direct,
+    nccl_version,
     predict_cost,
     sample_cells,
 )
 
-__all__ = ["Config", "FmmError", "Tree", "UnitCosts", "X", "choose_depth", "direct", "lib", "predict_cost", "sample_cells", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]
+__all__ = ["Comm", "nccl_version", "Config", "FmmError", "Tree", "UnitCosts", "X", "choose_depth", "direct", "lib", "predict_cost", "sample_cells", "library_path", "QUADTREE", "SEPTREE", "TRIQUAD"]

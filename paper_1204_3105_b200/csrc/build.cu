@@ -5,6 +5,8 @@
 //   lists       : P:101-111 Neighbors / NeighborsE4 (set-difference reading D1, from level 1: D2)
 #include <limits.h>
 
+#include <algorithm>
+
 #include "fmm_internal.cuh"
 #include "geometry.cuh"
 
@@ -387,6 +389,52 @@ __global__ void k_near(DGeo g, const int32_t* __restrict__ soff, const int32_t* 
   nnear[t] = k;
 }
 
+// ------------------------------------------------------------------ multi-rank selection
+// global leaf histogram of every rank's points (keys 0..K, K = out of domain)
+__global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[key[i]], 1);
+}
+
+// source leaves this rank keeps: its own leaf range [lo, hi) (it computes their P2M) and every
+// near source leaf of its own target leaves (the P2P halo)
+__global__ void k_halo_flags(int64_t lo, int64_t hi, const int32_t* __restrict__ gtoff,
+                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear,
+                             int32_t* __restrict__ flag) {
+  const int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= hi) return;
+  flag[t] = 1;
+  if (gtoff[t + 1] == gtoff[t]) return;
+  for (int q = 0; q < nnear[t]; ++q) flag[near[t * FMM_NEAR_MAX + q]] = 1;
+}
+
+// keep predicate of a point: its leaf is flagged (flag != NULL), else its leaf lies in [lo, hi)
+__device__ __forceinline__ int keep_point(uint32_t k, const int32_t* __restrict__ flag, int64_t lo, int64_t hi) {
+  return flag ? flag[k] : (int)((int64_t)k >= lo && (int64_t)k < hi);
+}
+__global__ void __launch_bounds__(256) k_keep(const uint32_t* __restrict__ key, int64_t n,
+                                              const int32_t* __restrict__ flag, int64_t lo, int64_t hi,
+                                              int32_t* __restrict__ f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) f[i] = keep_point(key[i], flag, lo, hi);
+}
+// stable compaction (input order kept, so the sort by key gives the (key, input index) order of
+// the single-rank tree); pos = exclusive scan of the predicate; *nout = kept count
+__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ key, int64_t n,
+                                                 const int32_t* __restrict__ flag, int64_t lo, int64_t hi,
+                                                 const int32_t* __restrict__ pos, uint32_t* __restrict__ ckey,
+                                                 int32_t* __restrict__ cidx, int64_t* __restrict__ nout) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = key[i];
+  const int kp = keep_point(k, flag, lo, hi);
+  if (kp) {
+    ckey[pos[i]] = k;
+    cidx[pos[i]] = (int32_t)i;
+  }
+  if (i == n - 1) *nout = (int64_t)pos[i] + kp;
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -417,9 +465,11 @@ static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
   return b;
 }
 
-// sort (key, iota) pairs stably; writes the permutation (sorted position -> input index)
-// and the leaf CSR off[0..K+1] from the sorted keys
-static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm, int32_t* off) {
+// sort (key, value) pairs stably, values = iota (vals0 == NULL) or vals0[i]; writes the
+// permutation (sorted position -> value, i.e. input index) and the leaf CSR off[0..K+1] from
+// the sorted keys
+static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32_t* perm, int32_t* off,
+                           const int32_t* vals0 = nullptr) {
   if (n == 0) {
     FMM_CUDA_TRY(cudaMemsetAsync(off, 0, sizeof(int32_t) * (t->g.K + 2), t->stream));
     return FMM_OK;
@@ -448,7 +498,7 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
   p += (size_t)nhist * 4;
   void* sscr = p;
   const uint32_t* kin = keys;
-  const int32_t* vin = nullptr;  // iota on the first pass
+  const int32_t* vin = vals0;  // iota on the first pass when NULL
   int shift = 0;
   for (int ps = 0; ps < passes; ++ps) {
     // balanced digit widths: the first (bits % passes) passes take one more bit
@@ -473,10 +523,74 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
   return FMM_OK;
 }
 
+// multi-rank: global leaf counts of every rank's points, near lists of every
+// leaf, the work-balanced leaf range of this rank (one host sync), its halo of near source
+// leaves, and the stable compaction of the points it keeps (a second host sync reads their
+// counts).  ckey / cidx (n + m entries each) receive the kept keys and input indices: sources
+// first, then targets (distinct-target trees).
+static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64_t* dcount) {
+  cudaStream_t s = t->stream;
+  const Geo& G = t->g;
+  const int64_t K = G.K;
+  // global histograms -> exclusive scans: gsoff[k] = #points with key < k, k = 0..K+1
+  const size_t sb = fmm_scan_scratch_bytes(K + 2);
+  void* sscr = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync(&sscr, sb, s));
+  FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (K + 2), s));
+  if (t->n > 0) k_hist<<<blocks_for(t->n, 256), 256, 0, s>>>(t->skey, t->n, t->gsoff);
+  int e = fmm_device_scan_i32(t->gsoff, t->gsoff, K + 2, sscr, sb, s, &t->launches);
+  if (!e && !G.self_mode) {
+    FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (K + 2), s));
+    if (t->m > 0) k_hist<<<blocks_for(t->m, 256), 256, 0, s>>>(t->tkey, t->m, t->gtoff);
+    e = fmm_device_scan_i32(t->gtoff, t->gtoff, K + 2, sscr, sb, s, &t->launches);
+  }
+  t->launches += G.self_mode ? 1 : 2;
+  cudaFreeAsync(sscr, s);
+  if (e) return e;
+  FMM_CUDA_TRY(cudaGetLastError());
+  // near lists (global emptiness) and the partition
+  e = fmm_stage_near_partition(t);
+  if (e) return e;
+  // halo flags of the source leaves, then stable compactions of the kept points
+  FMM_CUDA_TRY(cudaMemsetAsync(t->lflag, 0, sizeof(int32_t) * (K + 1), s));
+  if (t->leaf_hi > t->leaf_lo)
+    k_halo_flags<<<blocks_for(t->leaf_hi - t->leaf_lo, 128), 128, 0, s>>>(t->leaf_lo, t->leaf_hi, t->gtoff,
+                                                                          t->near, t->nnear, t->lflag);
+  t->launches++;
+  const int64_t nm_max = std::max(t->n, G.self_mode ? (int64_t)0 : t->m);
+  int32_t* pos = nullptr;
+  const size_t psb = fmm_scan_scratch_bytes(nm_max);
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&pos, sizeof(int32_t) * (nm_max + 1) + psb, s));
+  auto compact = [&](const uint32_t* key, int64_t cnt, const int32_t* flag, uint32_t* ck, int32_t* ci,
+                     int64_t* nout) -> int {
+    if (cnt == 0) {
+      return cudaMemsetAsync(nout, 0, sizeof(int64_t), s) == cudaSuccess ? FMM_OK : FMM_ECUDA;
+    }
+    k_keep<<<blocks_for(cnt, 256), 256, 0, s>>>(key, cnt, flag, t->leaf_lo, t->leaf_hi, pos);
+    int ee = fmm_device_scan_i32(pos, pos, cnt, pos + nm_max + 1, psb, s, &t->launches);
+    if (ee) return ee;
+    k_compact<<<blocks_for(cnt, 256), 256, 0, s>>>(key, cnt, flag, t->leaf_lo, t->leaf_hi, pos, ck, ci, nout);
+    t->launches += 2;
+    return FMM_OK;
+  };
+  e = compact(t->skey, t->n, t->lflag, ckey, cidx, dcount);
+  if (!e && !G.self_mode) e = compact(t->tkey, t->m, nullptr, ckey + t->n, cidx + t->n, dcount + 1);
+  cudaFreeAsync(pos, s);
+  if (e) return e;
+  FMM_CUDA_TRY(cudaGetLastError());
+  int64_t h[2] = {0, 0};
+  FMM_CUDA_TRY(cudaMemcpyAsync(h, dcount, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FMM_CUDA_TRY(cudaStreamSynchronize(s));
+  t->n_loc = h[0];
+  t->m_loc = G.self_mode ? h[0] : h[1];
+  return FMM_OK;
+}
+
 int fmm_stage_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
+  const bool multi = t->cfg.nranks > 1;
   double2* rec = nullptr;  // (x, y, u, 0) per source, input order
   if (t->n > 0) {
     FMM_CUDA_TRY(cudaMallocAsync((void**)&rec, (size_t)t->n * 32, s));
@@ -489,20 +603,39 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
-  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain points)
-  int e = radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
-  if (!e && !G.self_mode) e = radix_sort_perm(t, t->tkey, t->m, t->tperm, t->toff);
+  // multi-rank: select the kept points first (compacted keys + input indices)
+  uint32_t* ckey = nullptr;
+  int32_t* cidx = nullptr;
+  int e = FMM_OK;
+  t->n_loc = t->n;
+  t->m_loc = t->m;
+  if (multi) {
+    const int64_t tot = t->n + (G.self_mode ? 0 : t->m);
+    char* buf = nullptr;
+    FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, (size_t)tot * 8 + 256, s));
+    ckey = (uint32_t*)buf;
+    cidx = (int32_t*)(buf + (size_t)tot * 4);
+    int64_t* dcount = (int64_t*)(buf + (size_t)tot * 8);
+    e = multi_rank_select(t, ckey, cidx, dcount);
+  }
+  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain kept points)
+  if (!e) e = multi ? radix_sort_perm(t, ckey, t->n_loc, t->sperm, t->soff, cidx)
+                    : radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
+  if (!e && !G.self_mode)
+    e = multi ? radix_sort_perm(t, ckey + t->n, t->m_loc, t->tperm, t->toff, cidx + t->n)
+              : radix_sort_perm(t, t->tkey, t->m, t->tperm, t->toff);
+  if (ckey) cudaFreeAsync(ckey, s);
   if (e) {
     if (rec) cudaFreeAsync(rec, s);
     return e;
   }
-  if (t->n > 0) {
-    k_gather_src<<<blocks_for(t->n, 256), 256, 0, s>>>(t->sperm, t->n, rec, t->sxy, t->su);
+  if (t->n_loc > 0) {
+    k_gather_src<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, rec, t->sxy, t->su);
     t->launches++;
-    cudaFreeAsync(rec, s);
   }
-  if (!G.self_mode && t->m > 0) {
-    k_gather_xy<<<blocks_for(t->m, 256), 256, 0, s>>>(t->tperm, t->m, (const double2*)t->tgt_xy_in, t->txy);
+  if (rec) cudaFreeAsync(rec, s);
+  if (!G.self_mode && t->m_loc > 0) {
+    k_gather_xy<<<blocks_for(t->m_loc, 256), 256, 0, s>>>(t->tperm, t->m_loc, (const double2*)t->tgt_xy_in, t->txy);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
@@ -545,7 +678,7 @@ int fmm_stage_near_partition(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
-  k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->soff, t->toff, t->near, t->nnear, 0, G.K);
+  k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear, 0, G.K);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   if (t->cfg.nranks <= 1) {
@@ -556,7 +689,7 @@ int fmm_stage_near_partition(fmm_tree_s* t) {
   int64_t nb = (G.K + FMM_PART_BLOCK - 1) / FMM_PART_BLOCK;
   double* bw = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync((void**)&bw, nb * sizeof(double), s));
-  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->soff, t->toff, t->near, t->nnear, G.p, bw);
+  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->gsoff, t->gtoff, t->near, t->nnear, G.p, bw);
   t->launches++;
   std::vector<double> hb(nb);
   cudaError_t ce = cudaMemcpyAsync(hb.data(), bw, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
@@ -575,9 +708,14 @@ int fmm_stage_tables_lists(fmm_tree_s* t) {
   for (int l = 0; l <= G.L + 1; ++l) lvo.off[l] = G.lvl_off[l];
   k_centres<<<blocks_for(G.lvl_off[G.L + 1], 256), 256, 0, s>>>(g, lvo, t->centre);
   t->launches++;
-  int e = fmm_stage_near_partition(t);
-  if (e) return e;
-  k_cand_level<<<blocks_for(G.lvl_off[G.L], 128), 128, 0, s>>>(g, lvo, t->soff, t->toff, t->cand, t->ncand,
+  // single rank: near lists now (the multi-rank build made them before its local sort)
+  if (t->cfg.nranks <= 1) {
+    int e = fmm_stage_near_partition(t);
+    if (e) return e;
+  }
+  // E4 candidates: source emptiness from the global counts, targets of this rank's range from
+  // the local (kept) target CSR
+  k_cand_level<<<blocks_for(G.lvl_off[G.L], 128), 128, 0, s>>>(g, lvo, t->gsoff, t->toff, t->cand, t->ncand,
                                                                 t->leaf_lo, t->leaf_hi);
   k_e4mask_level<<<blocks_for(G.lvl_off[G.L + 1] - G.lvl_off[1], 128), 128, 0, s>>>(
       g, lvo, t->toff, t->cand, t->ncand, t->e4mask, t->leaf_lo, t->leaf_hi);
@@ -595,8 +733,8 @@ __global__ void k_gather_u(const int32_t* __restrict__ perm, int64_t n, const do
 }  // namespace
 
 int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u) {
-  if (t->n == 0) return FMM_OK;
-  k_gather_u<<<blocks_for(t->n, 256), 256, 0, t->stream>>>(t->sperm, t->n, u, t->su);
+  if (t->n_loc == 0) return FMM_OK;
+  k_gather_u<<<blocks_for(t->n_loc, 256), 256, 0, t->stream>>>(t->sperm, t->n_loc, u, t->su);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;

@@ -106,6 +106,8 @@ int make_geo(const fmm_config* c, Geo* g) {
   if (!(fabs(c->root_x) + 2.0 * c->root_size < 1e20 && fabs(c->root_y) + 2.0 * c->root_size < 1e20))
     return FMM_EBADCFG;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return FMM_EBADCFG;
+  // a communicator must describe the same rank / size as the configuration
+  if (c->comm && (fmm_comm_nranks(c->comm) != c->nranks || fmm_comm_rank(c->comm) != c->rank)) return FMM_EBADCFG;
   for (int i = 0; i < 5; ++i)
     if (c->reserved[i]) return FMM_EBADCFG;
   if (c->flags & ~FMM_FLAG_TIMING) return FMM_EBADCFG;
@@ -176,6 +178,16 @@ void carve(fmm_tree_s* t, Arena& a) {
     t->toff = a.take<int32_t>(K + 2);
     t->txy = a.take<double2>(m + 1);
   }
+  // global leaf CSR: its own arrays only on a multi-rank tree (the local sort keeps a subset)
+  if (t->cfg.nranks > 1) {
+    t->gsoff = a.take<int32_t>(K + 2);
+    t->gtoff = G.self_mode ? t->gsoff : a.take<int32_t>(K + 2);
+    t->lflag = a.take<int32_t>(K + 1);
+  } else {
+    t->gsoff = t->soff;
+    t->gtoff = t->toff;
+    t->lflag = nullptr;
+  }
   t->centre = a.take<double2>(G.total_cells);
   t->cand = a.take<int32_t>(inner * FMM_CAND_MAX);
   t->ncand = a.take<int32_t>(inner);
@@ -196,15 +208,29 @@ void carve(fmm_tree_s* t, Arena& a) {
 }
 
 
-int free_tree(fmm_tree_s* t) {
-  if (!t) return FMM_OK;
+// device buffers of a tree, freed stream-ordered on its stream (the handle stays valid)
+void release_buffers(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   if (t->scratch) cudaFreeAsync(t->scratch, s);
-  for (int i = 0; i < 3; ++i)
+  t->scratch = nullptr;
+  t->scratch_bytes = 0;
+  for (int i = 0; i < 3; ++i) {
     if (t->staging[i]) cudaFreeAsync(t->staging[i], s);
+    t->staging[i] = nullptr;
+  }
   if (t->slab) cudaFreeAsync(t->slab, s);
+  t->slab = nullptr;
+  t->released = 1;
+}
+
+int free_tree(fmm_tree_s* t) {
+  if (!t) return FMM_OK;
+  release_buffers(t);
   for (int i = 0; i < 8; ++i)
     if (t->ev[i]) cudaEventDestroy(t->ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (t->xev[i]) cudaEventDestroy(t->xev[i]);
+  if (t->xstream) cudaStreamDestroy(t->xstream);
   delete t;
   return FMM_OK;
 }
@@ -371,6 +397,7 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   t->m = m;
   t->leaf_lo = 0;  // the rank's range is set by fmm_stage_near_partition
   t->leaf_hi = g.K;
+  t->comm = cfg->comm;
   cudaStream_t s = t->stream;
   // inputs
   e = stage_input(t, src_xy, (size_t)n * 16, 0, &t->src_xy_in);
@@ -446,7 +473,7 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
 }
 
 int fmm_set_strengths(fmm_tree_t t, const double* src_u, void* stream) {
-  if (!t || (t->n > 0 && !src_u)) return FMM_EBADCFG;
+  if (!t || t->released || (t->n > 0 && !src_u)) return FMM_EBADCFG;
   if (stream) t->stream = (cudaStream_t)stream;
   const double* u = nullptr;
   int e = stage_input(t, src_u, (size_t)t->n * 8, 1, &u);
@@ -454,12 +481,47 @@ int fmm_set_strengths(fmm_tree_t t, const double* src_u, void* stream) {
   return e;
 }
 
-int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
-  if (!t) return FMM_EBADCFG;
+// the first half of an evaluation: upward pass (own source leaves), the multipole all-reduce
+// on the side stream when a communicator is set, and the P2P pair kernel, which needs no
+// multipoles and so overlaps the exchange
+int fmm_evaluate_begin(fmm_tree_t t, void* stream) {
+  if (!t || t->released) return FMM_EBADCFG;
+  if (stream) t->stream = (cudaStream_t)stream;
+  cudaStream_t s = t->stream;
+  t->begun = 0;
+  if (t->m == 0) return FMM_OK;
+  if (t->timing) cudaEventRecord(t->ev[3], s);
+  int e = fmm_stage_upward(t);
+  if (!e) e = debug_sync(s, "upward");
+  if (t->timing) cudaEventRecord(t->ev[4], s);
+  if (!e && t->comm) {
+    if (!t->xstream) {
+      int lo = 0, hi = 0;
+      FMM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      FMM_CUDA_TRY(cudaStreamCreateWithPriority(&t->xstream, cudaStreamNonBlocking, hi));
+      for (int i = 0; i < 2; ++i) FMM_CUDA_TRY(cudaEventCreateWithFlags(&t->xev[i], cudaEventDisableTiming));
+    }
+    FMM_CUDA_TRY(cudaEventRecord(t->xev[0], s));
+    FMM_CUDA_TRY(cudaStreamWaitEvent(t->xstream, t->xev[0], 0));
+    const Geo& G = t->g;
+    e = fmm_comm_allreduce_sum_f64(t->comm, (double*)t->mp, (size_t)G.total_cells * (G.p + 1) * 2, t->xstream);
+    if (!e) FMM_CUDA_TRY(cudaEventRecord(t->xev[1], t->xstream));
+  }
+  if (!e) e = fmm_stage_p2p_pairs(t);
+  if (!e) e = debug_sync(s, "p2p pairs");
+  if (t->timing) cudaEventRecord(t->ev[7], s);
+  if (!e) t->begun = 1;
+  return e;
+}
+
+// the second half: (wait for the exchange) M2L + L2L over every level, near-field sums + L2P
+int fmm_evaluate_end(fmm_tree_t t, double* phi_out, void* stream) {
+  if (!t || t->released) return FMM_EBADCFG;
   if (stream) t->stream = (cudaStream_t)stream;
   cudaStream_t s = t->stream;
   if (t->m == 0) return FMM_OK;
-  if (!phi_out) return FMM_EBADCFG;
+  if (!phi_out || !t->begun) return FMM_EBADCFG;
+  t->begun = 0;
   bool dev = is_device_ptr(phi_out);
   double2* phi = (double2*)phi_out;
   double2* tmp = nullptr;
@@ -470,15 +532,12 @@ int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
     if (t->cfg.nranks > 1)
       FMM_CUDA_TRY(cudaMemcpyAsync(tmp, phi_out, (size_t)t->m * 16, cudaMemcpyHostToDevice, s));
   }
-  if (t->timing) cudaEventRecord(t->ev[3], s);
-  int e = fmm_stage_upward(t);
-  if (!e) e = debug_sync(s, "upward");
-  if (t->timing) cudaEventRecord(t->ev[4], s);
-  if (!e) e = fmm_stage_downward(t);
+  if (t->comm) FMM_CUDA_TRY(cudaStreamWaitEvent(s, t->xev[1], 0));
+  int e = fmm_stage_downward(t);
   if (!e) e = debug_sync(s, "downward");
   if (t->timing) cudaEventRecord(t->ev[5], s);
-  if (!e) e = fmm_stage_p2p(t, phi);
-  if (!e) e = debug_sync(s, "p2p");
+  if (!e) e = fmm_stage_p2p_finish(t, phi);
+  if (!e) e = debug_sync(s, "p2p finish");
   if (t->timing) cudaEventRecord(t->ev[6], s);
   t->eval_timed = t->timing;
   if (!e && !dev) FMM_CUDA_TRY(cudaMemcpyAsync(phi_out, tmp, (size_t)t->m * 16, cudaMemcpyDeviceToHost, s));
@@ -486,8 +545,28 @@ int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
   return e;
 }
 
+int fmm_evaluate(fmm_tree_t t, double* phi_out, void* stream) {
+  if (!t || t->released) return FMM_EBADCFG;
+  if (t->m > 0 && !phi_out) return FMM_EBADCFG;
+  if (t->cfg.nranks > 1 && !t->comm) {
+    fmm_set_error_message("fmm_evaluate: nranks > 1 needs cfg->comm (or fmm_evaluate_begin / _end with the "
+                          "multipole exchange done by the caller)");
+    return FMM_EBADCFG;
+  }
+  int e = fmm_evaluate_begin(t, stream);
+  if (!e) e = fmm_evaluate_end(t, phi_out, stream);
+  return e;
+}
+
+int fmm_multipole_buffer(fmm_tree_t t, void** dev_ptr, size_t* bytes) {
+  if (!t || t->released) return FMM_EBADCFG;
+  if (dev_ptr) *dev_ptr = (void*)t->mp;
+  if (bytes) *bytes = (size_t)t->g.total_cells * (t->g.p + 1) * sizeof(double2);
+  return FMM_OK;
+}
+
 int fmm_status(fmm_tree_t t) {
-  if (!t) return FMM_EBADCFG;
+  if (!t || t->released) return FMM_EBADCFG;
   FMM_CUDA_TRY(cudaStreamSynchronize(t->stream));
   DevStatus st;
   FMM_CUDA_TRY(cudaMemcpy(&st, t->status, sizeof(st), cudaMemcpyDeviceToHost));
@@ -497,7 +576,7 @@ int fmm_status(fmm_tree_t t) {
 }
 
 int64_t fmm_last_error_index(fmm_tree_t t) {
-  if (!t) return -1;
+  if (!t || t->released) return -1;
   if (cudaStreamSynchronize(t->stream) != cudaSuccess) return -1;
   DevStatus st;
   if (cudaMemcpy(&st, t->status, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
@@ -513,8 +592,9 @@ int fmm_set_timing(fmm_tree_t t, int32_t enable) {
   t->timing = enable;
   return FMM_OK;
 }
-/* evaluate-stage times of the last fmm_evaluate with timing on: {0, 0, 0, upward, downward, p2p}
- * (build stages are timed by the caller around fmm_build_tree) */
+/* stage times: {keys + sort, lists + tasks, P2P pair kernel, upward, downward (incl. the wait
+ * for the multipole exchange), pair kernel + near-field sums / L2P}; the evaluation order is
+ * upward (ev3 -> ev4), pairs (ev4 -> ev7), downward (ev7 -> ev5), finish (ev5 -> ev6) */
 int fmm_stage_times(fmm_tree_t t, float* ms6) {
   if (!t || !ms6) return FMM_EBADCFG;
   for (int i = 0; i < 6; ++i) ms6[i] = 0.f;
@@ -526,10 +606,12 @@ int fmm_stage_times(fmm_tree_t t, float* ms6) {
   }
   if (t->eval_timed) {
     FMM_CUDA_TRY(cudaEventSynchronize(t->ev[6]));
-    cudaEventElapsedTime(&ms6[2], t->ev[5], t->ev[7]);
+    float fin = 0.f;
+    cudaEventElapsedTime(&ms6[2], t->ev[4], t->ev[7]);
     cudaEventElapsedTime(&ms6[3], t->ev[3], t->ev[4]);
-    cudaEventElapsedTime(&ms6[4], t->ev[4], t->ev[5]);
-    cudaEventElapsedTime(&ms6[5], t->ev[5], t->ev[6]);
+    cudaEventElapsedTime(&ms6[4], t->ev[7], t->ev[5]);
+    cudaEventElapsedTime(&fin, t->ev[5], t->ev[6]);
+    ms6[5] = ms6[2] + fin;
   }
   return FMM_OK;
 }
@@ -544,6 +626,12 @@ int fmm_rank_range(fmm_tree_t t, int64_t* lo, int64_t* hi) {
 int64_t fmm_launch_count(fmm_tree_t t) { return t ? t->launches : -1; }
 
 void fmm_free(fmm_tree_t t) { free_tree(t); }
+
+int fmm_release(fmm_tree_t t) {
+  if (!t) return FMM_EBADCFG;
+  release_buffers(t);
+  return FMM_OK;
+}
 
 int fmm_direct(const double* src_xy, const double* src_u, int64_t n, const double* tgt_xy, int64_t m,
                int32_t self_mode, double* phi_out, void* stream) {
@@ -665,7 +753,7 @@ static int copy_host(const void* src, size_t bytes, void* host_buf, size_t cap, 
 }
 
 int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t bytes, size_t* needed) {
-  if (!t) return FMM_EBADCFG;
+  if (!t || t->released) return FMM_EBADCFG;
   FMM_CUDA_TRY(cudaStreamSynchronize(t->stream));
   const Geo& G = t->g;
   int64_t K = G.K;
@@ -676,8 +764,8 @@ int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t
   switch (what) {
     case FMM_X_SRC_KEYS: return copy_out(t->skey, (size_t)t->n * 4, host_buf, bytes, needed);
     case FMM_X_TGT_KEYS: return copy_out(t->tkey, (size_t)t->m * 4, host_buf, bytes, needed);
-    case FMM_X_SRC_PERM: return copy_out(t->sperm, (size_t)t->n * 4, host_buf, bytes, needed);
-    case FMM_X_TGT_PERM: return copy_out(t->tperm, (size_t)t->m * 4, host_buf, bytes, needed);
+    case FMM_X_SRC_PERM: return copy_out(t->sperm, (size_t)t->n_loc * 4, host_buf, bytes, needed);
+    case FMM_X_TGT_PERM: return copy_out(t->tperm, (size_t)t->m_loc * 4, host_buf, bytes, needed);
     case FMM_X_CENTRES:
       return copy_out(t->centre + G.lvl_off[level], (size_t)G.ncells[level] * 16, host_buf, bytes, needed);
     case FMM_X_MULTIPOLE:

@@ -50,8 +50,15 @@ struct fmm_tree_s {
   uint32_t* tkey;  // [m] (aliases skey in self mode)
   int32_t* sperm;  // [n] sorted position -> input index
   int32_t* tperm;  // [m]
-  int32_t* soff;   // [K+2]
+  int32_t* soff;   // [K+2] leaf CSR of the sorted (rank-local) sources
   int32_t* toff;   // [K+2]
+  // global leaf CSR (every rank's points; multi-rank: histogram + scan before the rank-local
+  // sort; single rank: aliases soff / toff).  Emptiness tests of the lists and the work
+  // estimate of the partition use these; data access uses the local soff / toff.
+  int32_t* gsoff;  // [K+2]
+  int32_t* gtoff;  // [K+2]
+  int32_t* lflag;  // [K+1] multi-rank: source leaf kept by this rank (own range U near halo)
+  int64_t n_loc, m_loc;  // sorted (kept) sources / targets of this rank (= n, m on one rank)
   // sorted data
   double2* sxy;    // [n]
   double* su;      // [n]
@@ -76,8 +83,12 @@ struct fmm_tree_s {
   double* binom;   // [(2P+1)][(2P+1)] binomial table
   // status
   DevStatus* status;
-  // multi-rank leaf range
+  // multi-rank leaf range and the multipole exchange
   int64_t leaf_lo, leaf_hi;
+  fmm_comm_t comm;
+  cudaStream_t xstream;   // high-priority side stream of the all-reduce (created on first use)
+  cudaEvent_t xev[2];     // upward done (main -> side), all-reduce done (side -> main)
+  int begun;              // fmm_evaluate_begin enqueued, fmm_evaluate_end pending
   // timing
   int timing, build_timed, eval_timed;
   cudaEvent_t ev[8];
@@ -85,6 +96,7 @@ struct fmm_tree_s {
   int64_t launches;
   void* slab;  // single allocation holding every tree buffer
   size_t slab_bytes;
+  int released;  // fmm_release: device buffers returned to the pool, timings kept
   // scratch for sort
   void* scratch;
   size_t scratch_bytes;
@@ -106,13 +118,18 @@ void fmm_set_error_message(const std::string& s);
 int fmm_stage_keys_sort(fmm_tree_s* t);
 int fmm_stage_near_partition(fmm_tree_s* t);
 int fmm_stage_tables_lists(fmm_tree_s* t);
+// comm.cu
+int fmm_comm_allreduce_sum_f64(fmm_comm_t c, double* buf, size_t count, cudaStream_t s);
+int32_t fmm_comm_nranks(fmm_comm_t c);
+int32_t fmm_comm_rank(fmm_comm_t c);
 int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
                         cudaStream_t s, int64_t* launches);
 size_t fmm_scan_scratch_bytes(int64_t n);
 // passes.cu
 int fmm_stage_upward(fmm_tree_s* t);
 int fmm_stage_downward(fmm_tree_s* t);
-int fmm_stage_p2p(fmm_tree_s* t, double2* phi_out);
+int fmm_stage_p2p_pairs(fmm_tree_s* t);
+int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi_out);
 int fmm_build_tasks(fmm_tree_s* t);
 int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);
 int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s);

@@ -587,7 +587,7 @@ int fmm_build_tasks(fmm_tree_s* t) {
   return e;
 }
 
-int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
+int fmm_stage_p2p_pairs(fmm_tree_s* t) {
   const Geo& G = t->g;
   cudaStream_t s = t->stream;
   FMM_CUDA_TRY(cudaMemsetAsync(t->next_task, 0, sizeof(int32_t), s));
@@ -605,7 +605,14 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
   };
   int e = G.self_mode ? launch(k_p2p_pairs<true>) : launch(k_p2p_pairs<false>);
   if (e) return e;
-  if (t->timing) cudaEventRecord(t->ev[7], s);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
+int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi) {
+  const Geo& G = t->g;
+  cudaStream_t s = t->stream;
   const int64_t nl = t->leaf_hi - t->leaf_lo;
   if (nl > 0)
     switch (G.nslot) {
@@ -621,7 +628,7 @@ int fmm_stage_p2p(fmm_tree_s* t, double2* phi) {
 #undef FMM_FINISH
       default: return FMM_EBADCFG;
     }
-  t->launches += 2;
+  t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }

@@ -45,11 +45,15 @@ __device__ __forceinline__ double2 clog_principal(double dx, double dy) {
 template <int P>
 __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, const double* __restrict__ su,
                                              const int32_t* __restrict__ soff, const double2* __restrict__ cen,
-                                             int64_t K, int p, double2* __restrict__ mp) {
+                                             int64_t K, int64_t own_lo, int64_t own_hi, int p,
+                                             double2* __restrict__ mp) {
   const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / P2M_LPL;
   const int sub = threadIdx.x & (P2M_LPL - 1);
   const bool lvalid = leaf < K;
-  const int s0 = lvalid ? soff[leaf] : 0, s1 = lvalid ? soff[leaf + 1] : 0;
+  // multi-rank: only this rank's own source leaves (the halo leaves it keeps for P2P belong to
+  // other ranks' partial trees); every leaf is written, the others with zeros
+  const bool own = lvalid && leaf >= own_lo && leaf < own_hi;
+  const int s0 = own ? soff[leaf] : 0, s1 = own ? soff[leaf + 1] : 0;
   const double2 c = lvalid ? cen[leaf] : make_double2(0.0, 0.0);
   double Sr[P + 1], Si[P + 1];
 #pragma unroll
@@ -237,8 +241,10 @@ __global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int
 template <int P>
 void launch_p2m(fmm_tree_s* t) {
   const Geo& G = t->g;
+  const bool multi = t->cfg.nranks > 1;
   k_p2m<P><<<(unsigned)((G.K * P2M_LPL + 127) / 128), 128, 0, t->stream>>>(
-      t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], G.K, G.p, t->mp + G.lvl_off[G.L] * (G.p + 1));
+      t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], G.K, multi ? t->leaf_lo : 0, multi ? t->leaf_hi : G.K, G.p,
+      t->mp + G.lvl_off[G.L] * (G.p + 1));
 }
 
 }  // namespace

@@ -35,12 +35,16 @@ _DTYPE = {X.SRC_KEYS: np.uint32, X.TGT_KEYS: np.uint32, X.SRC_PERM: np.int32, X.
 class Config(C.Structure):
     _fields_ = [("tiling", C.c_int32), ("depth", C.c_int32), ("p", C.c_int32), ("self_mode", C.c_int32),
                 ("root_x", C.c_double), ("root_y", C.c_double), ("root_size", C.c_double),
-                ("rank", C.c_int32), ("nranks", C.c_int32), ("flags", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("flags", C.c_int32), ("reserved", C.c_int32 * 5),
+                ("comm", C.c_void_p)]
 
     @classmethod
-    def make(cls, tiling, depth, p, root_x, root_y, root_size, self_mode=False, rank=0, nranks=1, timing=False):
-        return cls(_TILING[tiling], int(depth), int(p), int(bool(self_mode)), float(root_x), float(root_y),
-                   float(root_size), int(rank), int(nranks), FLAG_TIMING if timing else 0)
+    def make(cls, tiling, depth, p, root_x, root_y, root_size, self_mode=False, rank=0, nranks=1, timing=False,
+             comm=None):
+        c = cls(_TILING[tiling], int(depth), int(p), int(bool(self_mode)), float(root_x), float(root_y),
+                float(root_size), int(rank), int(nranks), FLAG_TIMING if timing else 0)
+        c.comm = None if comm is None else comm.h
+        return c
 
 
 class FmmError(RuntimeError):
@@ -71,6 +75,13 @@ def lib():
         sig = {
             "fmm_build_tree": (C.c_int, [P(Config), vp, vp, C.c_int64, vp, C.c_int64, vp, P(vp)]),
             "fmm_evaluate": (C.c_int, [vp, vp, vp]),
+            "fmm_evaluate_begin": (C.c_int, [vp, vp]),
+            "fmm_evaluate_end": (C.c_int, [vp, vp, vp]),
+            "fmm_multipole_buffer": (C.c_int, [vp, P(vp), P(C.c_size_t)]),
+            "fmm_comm_unique_id": (C.c_int, [vp]),
+            "fmm_comm_init": (C.c_int, [vp, C.c_int32, C.c_int32, P(vp)]),
+            "fmm_comm_destroy": (C.c_int, [vp]),
+            "fmm_nccl_version": (C.c_int, []),
             "fmm_set_strengths": (C.c_int, [vp, vp, vp]),
             "fmm_status": (C.c_int, [vp]),
             "fmm_last_error_index": (C.c_int64, [vp]),
@@ -87,6 +98,7 @@ def lib():
                                            P(C.c_double)]),
             "fmm_choose_depth": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int32, vp, P(C.c_int32)]),
             "fmm_free": (None, [vp]),
+            "fmm_release": (C.c_int, [vp]),
             "fmm_error_string": (C.c_char_p, [C.c_int]),
             "fmm_last_error_message": (C.c_char_p, []),
             "fmm_version": (C.c_int, []),
@@ -145,6 +157,12 @@ class Tree:
             raise FmmError(rc, "fmm_build_tree")
         self.h = h
 
+    def release(self):
+        """fmm_release: device buffers back to the pool (stream-ordered); timings stay readable"""
+        rc = lib().fmm_release(self.h)
+        if rc:
+            raise FmmError(rc, "fmm_release")
+
     def close(self):
         if getattr(self, "h", None):
             lib().fmm_free(self.h)
@@ -168,6 +186,35 @@ class Tree:
         if rc:
             raise FmmError(rc, "fmm_evaluate")
         return out
+
+    def evaluate_begin(self, stream=None):
+        """fmm_evaluate_begin: upward pass over this rank's own leaves (+ the all-reduce when the
+        config has a comm) and the P2P pair kernel"""
+        st = _stream_ptr(stream) if stream is not None else self._stream
+        rc = lib().fmm_evaluate_begin(self.h, st)
+        if rc:
+            raise FmmError(rc, "fmm_evaluate_begin")
+
+    def evaluate_end(self, out=None, stream=None):
+        """fmm_evaluate_end: downward pass, near-field sums and L2P into `out`"""
+        if out is None:
+            import torch
+
+            out = torch.zeros(self.m, dtype=torch.complex128, device="cuda")
+        po, ko = _ptr(out)
+        st = _stream_ptr(stream) if stream is not None else self._stream
+        rc = lib().fmm_evaluate_end(self.h, po, st)
+        if rc:
+            raise FmmError(rc, "fmm_evaluate_end")
+        return out
+
+    def multipole_buffer(self):
+        """(device pointer, bytes) of the multipole tree (fmm_multipole_buffer)"""
+        p, nb = C.c_void_p(), C.c_size_t()
+        rc = lib().fmm_multipole_buffer(self.h, C.byref(p), C.byref(nb))
+        if rc:
+            raise FmmError(rc, "fmm_multipole_buffer")
+        return p.value, nb.value
 
     def set_strengths(self, u, stream=None):
         pu, ku = _ptr(u)
@@ -216,6 +263,40 @@ class Tree:
     def nbytes(self):
         """device bytes of the tree's slab (fmm_tree_bytes)"""
         return int(lib().fmm_tree_bytes(self.h))
+
+
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """fmm_comm_t: the library's NCCL communicator for one rank (current CUDA device)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        rc = lib().fmm_comm_unique_id(buf)
+        if rc:
+            raise FmmError(rc, "fmm_comm_unique_id")
+        return buf.raw
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != COMM_ID_BYTES:
+            raise ValueError("unique id must be 128 bytes")
+        h = C.c_void_p()
+        rc = lib().fmm_comm_init(C.create_string_buffer(uid, COMM_ID_BYTES), int(nranks), int(rank), C.byref(h))
+        if rc:
+            raise FmmError(rc, "fmm_comm_init")
+        self.h = h.value
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fmm_comm_destroy(self.h)
+            self.h = None
+
+
+def nccl_version() -> int:
+    return int(lib().fmm_nccl_version())
 
 
 def pool_reserve(nbytes: int):
