@@ -10,10 +10,13 @@ points, p = 24, seed 3) -- the configuration the metric is quoted on.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C3|C5|C1|C2]
   python bench.py --impl reference ...     (the CPU oracle, bounded sample)
 
-Multi-GPU (torchrun, one process per GPU): every rank gets the full input
-(replicated), builds the tree and the upward pass redundantly and evaluates its
-own range of target leaves (no data-path collective: DESIGN.md "Multi-GPU");
-time = max over ranks; value = all targets / time (strong scaling).
+Multi-GPU (one process per GPU; `--gpus N` without a launcher starts N ranks
+itself): every rank gets the full input (replicated), keys every point, takes a
+work-balanced contiguous range of leaves, sorts only its own + halo leaves, runs
+P2M / M2M over its own leaves and sums the multipole tree over the ranks with one
+ncclAllReduce on the library's communicator (overlapped with the P2P pair
+kernel), then evaluates its own targets (DESIGN.md §8); time = max over ranks;
+value = all targets / time (strong scaling: the 16.8M-point problem is fixed).
 """
 from __future__ import annotations
 
@@ -138,9 +141,18 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    comm = None
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the library's own NCCL communicator (the multipole all-reduce inside fmm_evaluate):
+        # rank 0's unique id reaches every rank through a torch.distributed broadcast
+        uid = torch.zeros(fmm.native.COMM_ID_BYTES, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(fmm.Comm.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = fmm.Comm(bytes(uid.cpu().numpy().tobytes()), world, rank)
+        log(f"[bench] rank {rank}/{world}: NCCL {fmm.nccl_version()} communicator ready")
     dev = torch.device("cuda", local)
     names = WORKLOADS[args.workload]
     inputs = make_inputs(names)
@@ -148,7 +160,7 @@ def run_gpu(args):
 
     def cfg_of(w, timing=False):
         return fmm.Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, w.self_mode,
-                               rank=rank, nranks=world, timing=timing)
+                               rank=rank, nranks=world, timing=timing, comm=comm)
 
     # device-resident inputs and outputs
     dev_in, host_in, outs, host_out = {}, {}, {}, {}
@@ -275,6 +287,8 @@ def run_gpu(args):
 
     if rank != 0:
         if world > 1:
+            dist.barrier()
+            comm.close()
             dist.destroy_process_group()
         return None
 
@@ -336,6 +350,8 @@ def run_gpu(args):
     if not args.no_cpu_baseline and world == 1:
         res["cpu_baseline"] = cpu_baseline(args, names, sample_targets=args.cpu_sample)
     if world > 1:
+        dist.barrier()
+        comm.close()
         dist.destroy_process_group()
     return res
 

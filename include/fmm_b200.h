@@ -193,6 +193,11 @@ int fmm_export(fmm_tree_t t, int32_t what, int32_t level, void* host_buf, size_t
  * P2M + M2M, M2L + L2L (all levels), P2P pair kernel + final sum/L2P}. */
 int fmm_set_timing(fmm_tree_t t, int32_t enable);
 int fmm_stage_times(fmm_tree_t t, float* ms6);
+/* Build stage times (ms, FMM_FLAG_TIMING): {keying of every point, multi-rank selection (global
+ * leaf counts, near lists, partition, halo, compaction; 0 on one rank), sort + gather of the
+ * kept points, centres + E4 lists + P2P tasks}.  The first two are the work every rank repeats
+ * on all points. */
+int fmm_build_times(fmm_tree_t t, float* ms4);
 
 /* Leaf range [lo, hi) of target leaves evaluated by cfg->rank (balanced by the
  * estimated near-field work; requires a built tree for the counts). */

@@ -35,7 +35,8 @@ namespace {
 __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
                                               int64_t index_base, uint32_t* __restrict__ key, DevStatus* st,
                                               const double* __restrict__ u = nullptr,
-                                              double2* __restrict__ rec = nullptr) {
+                                              double2* __restrict__ rec = nullptr,
+                                              int32_t* __restrict__ hist = nullptr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 p = xy[i];
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
     atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
   }
   key[i] = k;
+  if (hist) atomicAdd(&hist[k], 1);  // multi-rank: global leaf histogram of every point
 }
 
 // leaf CSR from the sorted keys: off[k] = #points with key < k, k = 0..K+1; position i
@@ -246,6 +248,17 @@ __global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const 
   sxy[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
   su[i] = w.x;
 }
+// multi-rank: the kept sources gathered straight from the caller's arrays (no packed record:
+// the rank keeps ~1/R of the points, so writing a record for every point would cost more)
+__global__ void k_gather_src_in(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
+                                const double* __restrict__ u, double2* __restrict__ sxy, double* __restrict__ su) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+  const double2 v = xy[j];
+  sxy[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
+  su[i] = u[j];
+}
 __global__ void k_gather_xy(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
                             double2* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -369,14 +382,8 @@ __global__ void k_e4mask_level(DGeo g, LevelOffsets lvo, const int32_t* __restri
 }
 
 // near(t) = ({t} U Neighbors(t, L)) with sources, ascending
-__global__ void k_near(DGeo g, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
-                       int32_t* __restrict__ near, int32_t* __restrict__ nnear, int64_t leaf_lo, int64_t leaf_hi) {
-  int64_t t = leaf_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= leaf_hi) return;
-  if (toff[t + 1] - toff[t] == 0) {
-    nnear[t] = 0;
-    return;
-  }
+__device__ void near_of(const DGeo& g, int64_t t, const int32_t* __restrict__ soff, int32_t* __restrict__ near,
+                        int32_t* __restrict__ nnear) {
   int64_t nb[17];
   int nn = geo_neighbors(g, g.L, t, nb);
   nb[nn++] = t;
@@ -389,18 +396,24 @@ __global__ void k_near(DGeo g, const int32_t* __restrict__ soff, const int32_t* 
   nnear[t] = k;
 }
 
-// ------------------------------------------------------------------ multi-rank selection (DESIGN.md §8)
-// global leaf histogram of every rank's points (keys 0..K, K = out of domain)
-__global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cnt) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(&cnt[key[i]], 1);
+__global__ void k_near(DGeo g, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                       int32_t* __restrict__ near, int32_t* __restrict__ nnear, int64_t leaf_lo, int64_t leaf_hi) {
+  int64_t t = leaf_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= leaf_hi) return;
+  if (toff[t + 1] - toff[t] == 0) {
+    nnear[t] = 0;
+    return;
+  }
+  near_of(g, t, soff, near, nnear);
 }
 
+// ------------------------------------------------------------------ multi-rank selection (DESIGN.md §8)
 // source leaves this rank keeps: its own leaf range [lo, hi) (it computes their P2M) and every
-// near source leaf of its own target leaves (the P2P halo)
+// near source leaf of its own target leaves (the P2P halo); byte flags (idempotent
+// stores), packed to a bitmask below
 __global__ void k_halo_flags(int64_t lo, int64_t hi, const int32_t* __restrict__ gtoff,
                              const int32_t* __restrict__ near, const int32_t* __restrict__ nnear,
-                             int32_t* __restrict__ flag) {
+                             uint8_t* __restrict__ flag) {
   const int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= hi) return;
   flag[t] = 1;
@@ -408,31 +421,147 @@ __global__ void k_halo_flags(int64_t lo, int64_t hi, const int32_t* __restrict__
   for (int q = 0; q < nnear[t]; ++q) flag[near[t * FMM_NEAR_MAX + q]] = 1;
 }
 
-// keep predicate of a point: its leaf is flagged (flag != NULL), else its leaf lies in [lo, hi)
-__device__ __forceinline__ int keep_point(uint32_t k, const int32_t* __restrict__ flag, int64_t lo, int64_t hi) {
-  return flag ? flag[k] : (int)((int64_t)k >= lo && (int64_t)k < hi);
-}
-__global__ void __launch_bounds__(256) k_keep(const uint32_t* __restrict__ key, int64_t n,
-                                              const int32_t* __restrict__ flag, int64_t lo, int64_t hi,
-                                              int32_t* __restrict__ f) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) f[i] = keep_point(key[i], flag, lo, hi);
-}
-// stable compaction (input order kept, so the sort by key gives the (key, input index) order of
-// the single-rank tree); pos = exclusive scan of the predicate; *nout = kept count
-__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ key, int64_t n,
-                                                 const int32_t* __restrict__ flag, int64_t lo, int64_t hi,
-                                                 const int32_t* __restrict__ pos, uint32_t* __restrict__ ckey,
-                                                 int32_t* __restrict__ cidx, int64_t* __restrict__ nout) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t k = key[i];
-  const int kp = keep_point(k, flag, lo, hi);
-  if (kp) {
-    ckey[pos[i]] = k;
-    cidx[pos[i]] = (int32_t)i;
+// every leaf t in [0, K): pack the keep flags into the bitmask (one word per warp), and give the
+// halo leaves outside [lo, hi) their near lists (the P2P tasks of symmetric blocks start from
+// the smaller leaf, which may be a halo leaf); leaves neither own nor halo get empty lists
+__global__ void __launch_bounds__(256) k_near_halo(DGeo g, int64_t K, int64_t lo, int64_t hi,
+                                                   const int32_t* __restrict__ gsoff,
+                                                   const int32_t* __restrict__ gtoff,
+                                                   const uint8_t* __restrict__ flag, int32_t* __restrict__ near,
+                                                   int32_t* __restrict__ nnear, uint32_t* __restrict__ bits) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool f = t <= K && flag[t];
+  const unsigned word = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && t <= K) bits[t >> 5] = word;
+  if (t >= K || (t >= lo && t < hi)) return;
+  if (!f || gtoff[t + 1] == gtoff[t]) {
+    nnear[t] = 0;
+    return;
   }
-  if (i == n - 1) *nout = (int64_t)pos[i] + kp;
+  near_of(g, t, gsoff, near, nnear);
+}
+
+// Stable single-pass compaction of the kept points (input order, so that the sort by key then
+// gives the (key, input index) order of the single-rank tree).  Keep predicate: the point's
+// leaf bit is set (bits != NULL: sources), else its leaf lies in [lo, hi) (distinct targets).
+// Tiles of CP_TILE keys are taken in ticket order; each publishes its kept count and finds its
+// output offset by a decoupled look-back over the earlier tiles' status words (state in bits
+// 62-63: 1 = tile count, 2 = inclusive prefix).  The leaf bitmask (32 KB for 2^18 leaves) sits in
+// shared memory when it fits, so the per-point lookups do not go to L2.
+constexpr int CP_T = 256, CP_V = 16, CP_TILE = CP_T * CP_V;
+constexpr unsigned long long CP_AGG = 1ull << 62, CP_INC = 2ull << 62, CP_CNT = (1ull << 62) - 1;
+__global__ void __launch_bounds__(CP_T) k_select_compact(const uint32_t* __restrict__ key, int64_t n,
+                                                         const uint32_t* __restrict__ bits, int nwords_smem,
+                                                         int64_t lo, int64_t hi, unsigned long long* tstat,
+                                                         int32_t* ticket, uint32_t* __restrict__ ckey,
+                                                         int32_t* __restrict__ cidx, int64_t* __restrict__ nout) {
+  extern __shared__ uint32_t s_bits[];
+  __shared__ int s_tile;
+  __shared__ int s_warp[CP_T / 32];
+  __shared__ long long s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // persistent blocks: the bitmask is staged once per block, tiles are taken by ticket
+  for (int i = tid; i < nwords_smem; i += CP_T) s_bits[i] = bits[i];
+  const uint32_t* bt = nwords_smem > 0 ? s_bits : bits;
+  const int64_t ntiles = (n + CP_TILE - 1) / CP_TILE;
+  while (true) {
+    __syncthreads();  // s_bits staged / the previous tile's shared words consumed
+    if (tid == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= ntiles) break;
+    const int64_t base = (int64_t)tile * CP_TILE + (int64_t)tid * CP_V;
+    uint32_t k[CP_V];
+    unsigned keep = 0;
+    if (base + CP_V <= n) {
+      const uint4* kp = (const uint4*)(key + base);
+#pragma unroll
+      for (int v = 0; v < CP_V / 4; ++v) {
+        const uint4 q = kp[v];
+        k[4 * v] = q.x, k[4 * v + 1] = q.y, k[4 * v + 2] = q.z, k[4 * v + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < CP_V; ++v) k[v] = base + v < n ? key[base + v] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int v = 0; v < CP_V; ++v) {
+      bool kp;
+      if (k[v] == 0xffffffffu) kp = false;
+      else if (bits) kp = (bt[k[v] >> 5] >> (k[v] & 31)) & 1u;
+      else kp = (int64_t)k[v] >= lo && (int64_t)k[v] < hi;
+      keep |= (unsigned)kp << v;
+    }
+    // block exclusive scan of the per-thread kept counts
+    const int c = __popc(keep);
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int i = 0; i < CP_T / 32; ++i) {
+      if (i < w) wbase += s_warp[i];
+      total += s_warp[i];
+    }
+    const int excl = wbase + x - c;
+    // decoupled look-back by warp 0: 32 earlier tiles per round, summing counts down to the
+    // nearest tile that has published its inclusive prefix
+    if (w == 0) {
+      if (lane == 0) atomicExch(&tstat[tile], (tile == 0 ? CP_INC : CP_AGG) | (unsigned long long)total);
+      long long prefix = 0;
+      for (int64_t j = tile - 1; j >= 0; j -= 32) {
+        const int64_t idx = j - lane;
+        unsigned long long v = CP_INC;  // before tile 0: an inclusive prefix of 0
+        if (idx >= 0) {
+          do {
+            v = *(volatile unsigned long long*)&tstat[idx];
+          } while ((v >> 62) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int first = inc ? __ffs(inc) - 1 : 32;
+        long long c_ = lane <= first ? (long long)(v & CP_CNT) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c_ += __shfl_xor_sync(0xffffffffu, c_, o);
+        prefix += c_;
+        if (inc) break;
+      }
+      if (lane == 0) {
+        if (tile > 0) atomicExch(&tstat[tile], CP_INC | (unsigned long long)(prefix + total));
+        s_prefix = prefix;
+        if (tile == ntiles - 1) *nout = prefix + total;
+      }
+    }
+    __syncthreads();
+    int64_t pos = s_prefix + excl;
+#pragma unroll
+    for (int v = 0; v < CP_V; ++v)
+      if ((keep >> v) & 1u) {
+        ckey[pos] = k[v];
+        cidx[pos] = (int32_t)(base + v);
+        ++pos;
+      }
+  }
+}
+
+// leaf CSR of a rank-local sorted key set (which skips whole key ranges): off[k] = lower bound
+// of k in the sorted keys, k = 0..K+1 (binary search per leaf; k_offsets' one-thread gap fill
+// would serialise over the skipped ranges)
+__global__ void __launch_bounds__(256) k_offsets_search(const uint32_t* __restrict__ sorted, int64_t n, int64_t K,
+                                                        int32_t* __restrict__ off) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > K + 1) return;
+  int64_t a = 0, b = n;
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if ((int64_t)sorted[mid] < k) a = mid + 1;
+    else b = mid;
+  }
+  off[k] = (int32_t)a;
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -517,7 +646,10 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
     vin = vout;
     shift += db;
   }
-  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+  if (t->cfg.nranks > 1)
+    k_offsets_search<<<blocks_for(t->g.K + 2, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+  else
+    k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
@@ -532,51 +664,59 @@ static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   const int64_t K = G.K;
-  // global histograms -> exclusive scans: gsoff[k] = #points with key < k, k = 0..K+1
+  // global histograms (made by the keying kernels) -> exclusive scans: gsoff[k] = #points with
+  // key < k, k = 0..K+1
   const size_t sb = fmm_scan_scratch_bytes(K + 2);
   void* sscr = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync(&sscr, sb, s));
-  FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (K + 2), s));
-  if (t->n > 0) k_hist<<<blocks_for(t->n, 256), 256, 0, s>>>(t->skey, t->n, t->gsoff);
   int e = fmm_device_scan_i32(t->gsoff, t->gsoff, K + 2, sscr, sb, s, &t->launches);
-  if (!e && !G.self_mode) {
-    FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (K + 2), s));
-    if (t->m > 0) k_hist<<<blocks_for(t->m, 256), 256, 0, s>>>(t->tkey, t->m, t->gtoff);
-    e = fmm_device_scan_i32(t->gtoff, t->gtoff, K + 2, sscr, sb, s, &t->launches);
-  }
-  t->launches += G.self_mode ? 1 : 2;
+  if (!e && !G.self_mode) e = fmm_device_scan_i32(t->gtoff, t->gtoff, K + 2, sscr, sb, s, &t->launches);
   cudaFreeAsync(sscr, s);
   if (e) return e;
   FMM_CUDA_TRY(cudaGetLastError());
   // near lists (global emptiness) and the partition
   e = fmm_stage_near_partition(t);
   if (e) return e;
-  // halo flags of the source leaves, then stable compactions of the kept points
-  FMM_CUDA_TRY(cudaMemsetAsync(t->lflag, 0, sizeof(int32_t) * (K + 1), s));
+  // halo flags of the source leaves (bytes, then a bitmask with the halo near lists), then
+  // stable compactions of the kept points
+  const int64_t nwords = (K + 1 + 31) / 32;
+  uint32_t* bits = (uint32_t*)t->lflag;
+  uint8_t* flag8 = (uint8_t*)(bits + nwords);
+  FMM_CUDA_TRY(cudaMemsetAsync(flag8, 0, K + 1, s));
   if (t->leaf_hi > t->leaf_lo)
     k_halo_flags<<<blocks_for(t->leaf_hi - t->leaf_lo, 128), 128, 0, s>>>(t->leaf_lo, t->leaf_hi, t->gtoff,
-                                                                          t->near, t->nnear, t->lflag);
-  t->launches++;
-  const int64_t nm_max = std::max(t->n, G.self_mode ? (int64_t)0 : t->m);
-  int32_t* pos = nullptr;
-  const size_t psb = fmm_scan_scratch_bytes(nm_max);
-  FMM_CUDA_TRY(cudaMallocAsync((void**)&pos, sizeof(int32_t) * (nm_max + 1) + psb, s));
-  auto compact = [&](const uint32_t* key, int64_t cnt, const int32_t* flag, uint32_t* ck, int32_t* ci,
-                     int64_t* nout) -> int {
-    if (cnt == 0) {
-      return cudaMemsetAsync(nout, 0, sizeof(int64_t), s) == cudaSuccess ? FMM_OK : FMM_ECUDA;
-    }
-    k_keep<<<blocks_for(cnt, 256), 256, 0, s>>>(key, cnt, flag, t->leaf_lo, t->leaf_hi, pos);
-    int ee = fmm_device_scan_i32(pos, pos, cnt, pos + nm_max + 1, psb, s, &t->launches);
-    if (ee) return ee;
-    k_compact<<<blocks_for(cnt, 256), 256, 0, s>>>(key, cnt, flag, t->leaf_lo, t->leaf_hi, pos, ck, ci, nout);
-    t->launches += 2;
-    return FMM_OK;
-  };
-  e = compact(t->skey, t->n, t->lflag, ckey, cidx, dcount);
-  if (!e && !G.self_mode) e = compact(t->tkey, t->m, nullptr, ckey + t->n, cidx + t->n, dcount + 1);
-  cudaFreeAsync(pos, s);
-  if (e) return e;
+                                                                          t->near, t->nnear, flag8);
+  k_near_halo<<<blocks_for(K + 1, 256), 256, 0, s>>>(dgeo(G), K, t->leaf_lo, t->leaf_hi, t->gsoff, t->gtoff, flag8,
+                                                     t->near, t->nnear, bits);
+  t->launches += 2;
+  // the bitmask goes to shared memory when it fits (<= 160 KB: 1.3M leaves)
+  const int smem_words = nwords * 4 <= 160 * 1024 ? (int)nwords : 0;
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_select_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    std::max(smem_words * 4, 1)));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nt_s = (t->n + CP_TILE - 1) / CP_TILE;
+  const int64_t nt_t = G.self_mode ? 0 : (t->m + CP_TILE - 1) / CP_TILE;
+  unsigned long long* tstat = nullptr;  // tile status words of both compactions + 2 tickets
+  const size_t stat_bytes = sizeof(unsigned long long) * (nt_s + nt_t + 2);
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&tstat, stat_bytes, s));
+  FMM_CUDA_TRY(cudaMemsetAsync(tstat, 0, stat_bytes, s));
+  FMM_CUDA_TRY(cudaMemsetAsync(dcount, 0, 2 * sizeof(int64_t), s));
+  int32_t* tickets = (int32_t*)(tstat + nt_s + nt_t);
+  const unsigned grid_s = (unsigned)std::min<int64_t>(nt_s, 2 * nsm), grid_t = (unsigned)std::min<int64_t>(nt_t, 4 * nsm);
+  if (nt_s > 0) {
+    k_select_compact<<<grid_s, CP_T, smem_words * 4, s>>>(t->skey, t->n, bits, smem_words, 0, 0, tstat,
+                                                                  tickets, ckey, cidx, dcount);
+    t->launches++;
+  }
+  if (nt_t > 0) {
+    k_select_compact<<<grid_t, CP_T, 0, s>>>(t->tkey, t->m, nullptr, 0, t->leaf_lo, t->leaf_hi,
+                                                     tstat + nt_s, tickets + 1, ckey + t->n, cidx + t->n,
+                                                     dcount + 1);
+    t->launches++;
+  }
+  cudaFreeAsync(tstat, s);
   FMM_CUDA_TRY(cudaGetLastError());
   int64_t h[2] = {0, 0};
   FMM_CUDA_TRY(cudaMemcpyAsync(h, dcount, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -591,18 +731,24 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   const Geo& G = t->g;
   DGeo g = dgeo(G);
   const bool multi = t->cfg.nranks > 1;
-  double2* rec = nullptr;  // (x, y, u, 0) per source, input order
+  double2* rec = nullptr;  // (x, y, u, 0) per source, input order (one rank only)
+  if (multi) {
+    FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (G.K + 2), s));
+    if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (G.K + 2), s));
+  }
   if (t->n > 0) {
-    FMM_CUDA_TRY(cudaMallocAsync((void**)&rec, (size_t)t->n * 32, s));
+    if (!multi) FMM_CUDA_TRY(cudaMallocAsync((void**)&rec, (size_t)t->n * 32, s));
     k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->status,
-                                                  t->src_u_in, rec);
+                                                  multi ? nullptr : t->src_u_in, rec, multi ? t->gsoff : nullptr);
     t->launches++;
   }
   if (!G.self_mode && t->m > 0) {
-    k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->status);
+    k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->status,
+                                                  nullptr, nullptr, multi ? t->gtoff : nullptr);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
+  if (t->timing) cudaEventRecord(t->ev[8], s);
   // multi-rank: select the kept points first (compacted keys + input indices)
   uint32_t* ckey = nullptr;
   int32_t* cidx = nullptr;
@@ -618,6 +764,7 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
     int64_t* dcount = (int64_t*)(buf + (size_t)tot * 8);
     e = multi_rank_select(t, ckey, cidx, dcount);
   }
+  if (t->timing) cudaEventRecord(t->ev[9], s);
   // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain kept points)
   if (!e) e = multi ? radix_sort_perm(t, ckey, t->n_loc, t->sperm, t->soff, cidx)
                     : radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
@@ -630,7 +777,11 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
     return e;
   }
   if (t->n_loc > 0) {
-    k_gather_src<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, rec, t->sxy, t->su);
+    if (multi)
+      k_gather_src_in<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, (const double2*)t->src_xy_in,
+                                                                 t->src_u_in, t->sxy, t->su);
+    else
+      k_gather_src<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, rec, t->sxy, t->su);
     t->launches++;
   }
   if (rec) cudaFreeAsync(rec, s);
@@ -645,21 +796,20 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
 namespace {
 // estimated evaluation work of each leaf (P2P pairs + per-target L2P + per-leaf downward),
 // summed over blocks of FMM_PART_BLOCK leaves (the multi-rank partition)
-__global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
-                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int p,
-                             double* __restrict__ bw) {
+// The estimate uses the leaf's own counts: w_t = n_t^tgt * (n_t^src * P2) + 2 (p+1) n_t^tgt +
+// 40 (p+1)^2, i.e. the near field as if every near leaf held as many sources as t (exact
+// for uniform trees up to the boundary; the partition only needs a balance estimate, and it
+// then needs no near list of any leaf outside the rank's range and halo).
+__global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff, int p2,
+                             int p, double* __restrict__ bw) {
   __shared__ double warp_sum[FMM_PART_BLOCK / 32];
   int64_t leaf = blockIdx.x * (int64_t)FMM_PART_BLOCK + threadIdx.x;
   double w = 0.0;
   if (leaf < K) {
-    int nt = toff[leaf + 1] - toff[leaf];
+    const int nt = toff[leaf + 1] - toff[leaf];
     if (nt > 0) {
-      int64_t ns = 0;
-      for (int q = 0; q < nnear[leaf]; ++q) {
-        int sl = near[leaf * FMM_NEAR_MAX + q];
-        ns += soff[sl + 1] - soff[sl];
-      }
-      w = (double)nt * (double)ns + 2.0 * (p + 1) * nt + 40.0 * (p + 1) * (p + 1);
+      const int ns = soff[leaf + 1] - soff[leaf];
+      w = (double)nt * (double)ns * p2 + 2.0 * (p + 1) * nt + 40.0 * (p + 1) * (p + 1);
     }
   }
   for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
@@ -673,30 +823,39 @@ __global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const 
 }
 }  // namespace
 
-// near lists of every leaf; for nranks > 1 the work-balanced leaf range of this rank
+// one rank: near lists of every leaf.  nranks > 1: the work-balanced leaf range of this rank
+// (one host sync), then the near lists of its own leaves
 int fmm_stage_near_partition(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
-  k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear, 0, G.K);
-  t->launches++;
-  FMM_CUDA_TRY(cudaGetLastError());
   if (t->cfg.nranks <= 1) {
     t->leaf_lo = 0;
     t->leaf_hi = G.K;
+    k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear, 0, G.K);
+    t->launches++;
+    FMM_CUDA_TRY(cudaGetLastError());
     return FMM_OK;
   }
   int64_t nb = (G.K + FMM_PART_BLOCK - 1) / FMM_PART_BLOCK;
   double* bw = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync((void**)&bw, nb * sizeof(double), s));
-  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->gsoff, t->gtoff, t->near, t->nnear, G.p, bw);
+  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->gsoff, t->gtoff, G.nslot, G.p, bw);
   t->launches++;
   std::vector<double> hb(nb);
   cudaError_t ce = cudaMemcpyAsync(hb.data(), bw, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
   cudaFreeAsync(bw, s);
   FMM_CUDA_TRY(ce);
-  return fmm_partition(hb.data(), nb, FMM_PART_BLOCK, G.K, t->cfg.rank, t->cfg.nranks, &t->leaf_lo, &t->leaf_hi);
+  int e = fmm_partition(hb.data(), nb, FMM_PART_BLOCK, G.K, t->cfg.rank, t->cfg.nranks, &t->leaf_lo, &t->leaf_hi);
+  if (e) return e;
+  if (t->leaf_hi > t->leaf_lo) {
+    k_near<<<blocks_for(t->leaf_hi - t->leaf_lo, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear,
+                                                                   t->leaf_lo, t->leaf_hi);
+    t->launches++;
+  }
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
 }
 
 int fmm_stage_tables_lists(fmm_tree_s* t) {

@@ -226,7 +226,7 @@ void release_buffers(fmm_tree_s* t) {
 int free_tree(fmm_tree_s* t) {
   if (!t) return FMM_OK;
   release_buffers(t);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 10; ++i)
     if (t->ev[i]) cudaEventDestroy(t->ev[i]);
   for (int i = 0; i < 2; ++i)
     if (t->xev[i]) cudaEventDestroy(t->xev[i]);
@@ -588,7 +588,7 @@ int64_t fmm_last_error_index(fmm_tree_t t) {
 int fmm_set_timing(fmm_tree_t t, int32_t enable) {
   if (!t) return FMM_EBADCFG;
   if (enable && !t->ev[0])
-    for (int i = 0; i < 8; ++i) FMM_CUDA_TRY(cudaEventCreate(&t->ev[i]));
+    for (int i = 0; i < 10; ++i) FMM_CUDA_TRY(cudaEventCreate(&t->ev[i]));
   t->timing = enable;
   return FMM_OK;
 }
@@ -613,6 +613,18 @@ int fmm_stage_times(fmm_tree_t t, float* ms6) {
     cudaEventElapsedTime(&fin, t->ev[5], t->ev[6]);
     ms6[5] = ms6[2] + fin;
   }
+  return FMM_OK;
+}
+
+int fmm_build_times(fmm_tree_t t, float* ms4) {
+  if (!t || !ms4) return FMM_EBADCFG;
+  for (int i = 0; i < 4; ++i) ms4[i] = 0.f;
+  if (!t->timing || !t->build_timed) return FMM_OK;
+  FMM_CUDA_TRY(cudaEventSynchronize(t->ev[2]));
+  cudaEventElapsedTime(&ms4[0], t->ev[0], t->ev[8]);
+  cudaEventElapsedTime(&ms4[1], t->ev[8], t->ev[9]);
+  cudaEventElapsedTime(&ms4[2], t->ev[9], t->ev[1]);
+  cudaEventElapsedTime(&ms4[3], t->ev[1], t->ev[2]);
   return FMM_OK;
 }
 

@@ -57,7 +57,8 @@ struct fmm_tree_s {
   // estimate of the partition use these; data access uses the local soff / toff.
   int32_t* gsoff;  // [K+2]
   int32_t* gtoff;  // [K+2]
-  int32_t* lflag;  // [K+1] multi-rank: source leaf kept by this rank (own range U near halo)
+  int32_t* lflag;  // [K+1] multi-rank: bitmask ((K+32)/32 words, then K+1 byte flags) of the source leaves this rank
+                   // keeps (own range U near halo)
   int64_t n_loc, m_loc;  // sorted (kept) sources / targets of this rank (= n, m on one rank)
   // sorted data
   double2* sxy;    // [n]
@@ -91,7 +92,7 @@ struct fmm_tree_s {
   int begun;              // fmm_evaluate_begin enqueued, fmm_evaluate_end pending
   // timing
   int timing, build_timed, eval_timed;
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[10];  // 0-7 stages (capi.cu); 8 keys done, 9 multi-rank selection done (build.cu)
   float stage_ms[6];
   int64_t launches;
   void* slab;  // single allocation holding every tree buffer

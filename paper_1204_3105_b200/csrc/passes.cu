@@ -45,15 +45,14 @@ __device__ __forceinline__ double2 clog_principal(double dx, double dy) {
 template <int P>
 __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, const double* __restrict__ su,
                                              const int32_t* __restrict__ soff, const double2* __restrict__ cen,
-                                             int64_t K, int64_t own_lo, int64_t own_hi, int p,
-                                             double2* __restrict__ mp) {
-  const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / P2M_LPL;
+                                             int64_t own_lo, int64_t own_hi, int p, double2* __restrict__ mp) {
+  // leaves [own_lo, own_hi): every leaf on one rank; on a multi-rank tree this rank's own source
+  // leaves only (the halo leaves it keeps for P2P belong to other ranks' partial trees, and the
+  // rest of the multipole tree was zeroed)
+  const int64_t leaf = own_lo + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / P2M_LPL;
   const int sub = threadIdx.x & (P2M_LPL - 1);
-  const bool lvalid = leaf < K;
-  // multi-rank: only this rank's own source leaves (the halo leaves it keeps for P2P belong to
-  // other ranks' partial trees); every leaf is written, the others with zeros
-  const bool own = lvalid && leaf >= own_lo && leaf < own_hi;
-  const int s0 = own ? soff[leaf] : 0, s1 = own ? soff[leaf + 1] : 0;
+  const bool lvalid = leaf < own_hi;
+  const int s0 = lvalid ? soff[leaf] : 0, s1 = lvalid ? soff[leaf + 1] : 0;
   const double2 c = lvalid ? cen[leaf] : make_double2(0.0, 0.0);
   double Sr[P + 1], Si[P + 1];
 #pragma unroll
@@ -101,12 +100,13 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 // ------------------------------------------------------------------ M2M (one warp per parent, lane = coefficient)
 // a child's multipole is staged once in shared memory (one coalesced load), so that the
 // Horner loop of lane k reads a_j without a memory round trip per step
-__global__ void __launch_bounds__(128) k_m2m(int B, int64_t nparents, int64_t span_l, const int32_t* __restrict__ soff,
+__global__ void __launch_bounds__(128) k_m2m(int B, int64_t par0, int64_t nparents, int64_t span_l,
+                                             const int32_t* __restrict__ soff,
                                              const double2* __restrict__ cen_par, const double2* __restrict__ cen_ch,
                                              const double2* __restrict__ mp_ch, int p, const double* __restrict__ binom,
                                              double2* __restrict__ mp_par) {
   __shared__ double2 s_a[4][32];
-  const int64_t P = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t P = par0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // parents [par0, nparents)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (P >= nparents) return;
   const double2 cp = cen_par[P];
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(128) k_m2m(int B, int64_t nparents, int64_t sp
 //    b_l += w^l (sum_k C(l+k-1, k-1) a~_k - Q/l) with its binomial row C(l+k-1, k-1) held in
 //    registers; lane 0 adds Q Log(c_t - c_s) + sum_k a~_k.
 template <int P>
-__global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int64_t span_l,
+__global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t cell0, int64_t ncells, int64_t span_l,
                                                const int32_t* __restrict__ toff, int64_t leaf_lo, int64_t leaf_hi,
                                                const double2* __restrict__ cen_l, const double2* __restrict__ cen_par,
                                                const double2* __restrict__ loc_par, const int32_t* __restrict__ cand,
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int
   __shared__ double2 s_lg[4][NB];
   __shared__ double s_q[4][NB];
   __shared__ double2 s_at[4][32];
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
   if (t >= ncells) return;
   const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
@@ -241,18 +241,35 @@ __global__ void __launch_bounds__(128) k_down2(int l, int B, int64_t ncells, int
 template <int P>
 void launch_p2m(fmm_tree_s* t) {
   const Geo& G = t->g;
-  const bool multi = t->cfg.nranks > 1;
-  k_p2m<P><<<(unsigned)((G.K * P2M_LPL + 127) / 128), 128, 0, t->stream>>>(
-      t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], G.K, multi ? t->leaf_lo : 0, multi ? t->leaf_hi : G.K, G.p,
+  const int64_t nl = t->leaf_hi - t->leaf_lo;
+  if (nl <= 0) return;
+  k_p2m<P><<<(unsigned)((nl * P2M_LPL + 127) / 128), 128, 0, t->stream>>>(
+      t->sxy, t->su, t->soff, t->centre + G.lvl_off[G.L], t->leaf_lo, t->leaf_hi, G.p,
       t->mp + G.lvl_off[G.L] * (G.p + 1));
 }
 
 }  // namespace
 
+// cells [c0, c1) of level l that hold a leaf of this rank's range (every cell on one rank)
+static void level_range(const fmm_tree_s* t, int l, int64_t* c0, int64_t* c1) {
+  const Geo& G = t->g;
+  const int64_t span = G.ncells[G.L - l];  // B^(L-l)
+  if (t->leaf_hi <= t->leaf_lo) {
+    *c0 = *c1 = 0;
+    return;
+  }
+  *c0 = t->leaf_lo / span;
+  *c1 = (t->leaf_hi + span - 1) / span;
+}
+
 int fmm_stage_upward(fmm_tree_s* t) {
   const Geo& G = t->g;
   cudaStream_t s = t->stream;
   int p = G.p;
+  // multi-rank: the partial multipole tree is zero outside this rank's own cells (the all-reduce
+  // sums every rank's tree); P2M / M2M then run over the rank's cells only
+  if (t->cfg.nranks > 1)
+    FMM_CUDA_TRY(cudaMemsetAsync(t->mp, 0, sizeof(double2) * (size_t)G.total_cells * (p + 1), s));
   if (p <= 8) launch_p2m<8>(t);
   else if (p <= 12) launch_p2m<12>(t);
   else if (p <= 16) launch_p2m<16>(t);
@@ -262,9 +279,11 @@ int fmm_stage_upward(fmm_tree_s* t) {
   else launch_p2m<32>(t);
   t->launches++;
   for (int l = G.L - 1; l >= 1; --l) {
-    int64_t np = G.ncells[l];
-    k_m2m<<<(unsigned)((np * 32 + 127) / 128), 128, 0, s>>>(
-        G.B, np, G.ncells[G.L - l - 1] /* B^(L-l-1) */, t->soff, t->centre + G.lvl_off[l],
+    int64_t c0, c1;
+    level_range(t, l, &c0, &c1);
+    if (c1 <= c0) continue;
+    k_m2m<<<(unsigned)(((c1 - c0) * 32 + 127) / 128), 128, 0, s>>>(
+        G.B, c0, c1, G.ncells[G.L - l - 1] /* B^(L-l-1) */, t->soff, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l + 1], t->mp + G.lvl_off[l + 1] * (p + 1), p, t->binom, t->mp + G.lvl_off[l] * (p + 1));
     t->launches++;
   }
@@ -303,7 +322,8 @@ struct DownSmem {
 #define DOWN_MINB(P) ((P) >= 20 ? 4 : 5)  // resident blocks per SM (register budget 128 / 96)
 #endif
 template <int P>
-__global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, int64_t ncells, int64_t span_l,
+__global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, int64_t cell0, int64_t ncells,
+                                                     int64_t span_l,
                                                      const int32_t* __restrict__ toff, int64_t leaf_lo,
                                                      int64_t leaf_hi, const double2* __restrict__ cen_l,
                                                      const double2* __restrict__ cen_par,
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   for (int i = threadIdx.x; i < 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
   __syncthreads();
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // cells [cell0, ncells)
   if (t >= ncells) return;
   const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
   if (thi <= tlo || toff[thi] == toff[tlo]) return;  // no targets of this rank below t
@@ -464,20 +484,23 @@ template <int P>
 static void launch_down(fmm_tree_s* t, int l) {
   const Geo& G = t->g;
   const int p = G.p;
-  const int64_t nc = G.ncells[l];
+  int64_t c0, c1;
+  level_range(t, l, &c0, &c1);
+  if (c1 <= c0) return;
+  const int64_t nc = c1 - c0;
   static const bool simt = getenv("FMM_M2L_SIMT") && getenv("FMM_M2L_SIMT")[0] == '1';
   if (!simt) {
     // per device (a process may drive several GPUs); a failure surfaces as the launch error
     cudaFuncSetAttribute(k_down_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DownSmem<P>::bytes);
     k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, DownSmem<P>::bytes, t->stream>>>(
-        l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
+        l, G.B, c0, c1, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
         t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->p2p_tab,
         t->loc + G.lvl_off[l] * (p + 1));
     return;
   }
   k_down2<P><<<(unsigned)((nc * 32 + 127) / 128), 128, 0, t->stream>>>(
-      l, G.B, nc, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
+      l, G.B, c0, c1, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
       t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
       t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
 }

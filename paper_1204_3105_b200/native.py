@@ -88,6 +88,7 @@ def lib():
             "fmm_export": (C.c_int, [vp, C.c_int32, C.c_int32, vp, C.c_size_t, P(C.c_size_t)]),
             "fmm_set_timing": (C.c_int, [vp, C.c_int32]),
             "fmm_stage_times": (C.c_int, [vp, P(C.c_float)]),
+            "fmm_build_times": (C.c_int, [vp, P(C.c_float)]),
             "fmm_rank_range": (C.c_int, [vp, P(C.c_int64), P(C.c_int64)]),
             "fmm_launch_count": (C.c_int64, [vp]),
             "fmm_pool_reserve": (C.c_int, [C.c_size_t]),
@@ -250,6 +251,12 @@ class Tree:
     def stage_times(self):
         ms = (C.c_float * 6)()
         lib().fmm_stage_times(self.h, ms)
+        return list(ms)
+
+    def build_times(self):
+        """{keys, multi-rank selection, sort + gather, lists + tasks} in ms (fmm_build_times)"""
+        ms = (C.c_float * 4)()
+        lib().fmm_build_times(self.h, ms)
         return list(ms)
 
     def rank_range(self):
