@@ -205,6 +205,15 @@ def cell_index(cfg, x, y, level):
     return int(out.value)
 
 
+def keys_all(cfg, xy):
+    """keys of every point, out-of-domain points as 0xffffffff (no error raised)"""
+    xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+    k = np.zeros(len(xy), np.uint32)
+    bad = C.c_int64(-1)
+    lib().orc_keys(C.byref(cfg), _ptr(xy, _d), len(xy), _ptr(k, _u32), C.byref(bad))
+    return k
+
+
 def keys(cfg, xy):
     xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
     k = np.zeros(len(xy), np.uint32)

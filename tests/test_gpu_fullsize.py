@@ -71,15 +71,18 @@ def test_fullsize_lists_bit_exact(cache, name):
         assert np.array_equal(g.export(X.E4_ENTRIES, l), en), l
 
 
+def heavy_leaf_ids(o):
+    """input indices of every target of the most loaded leaf"""
+    _, to = o.leaf_offsets()
+    heavy = int(np.argmax(np.diff(to)))
+    _, tperm = o.perm()
+    return np.sort(tperm[to[heavy]:to[heavy + 1]].astype(np.int64))
+
+
 def sample_ids(w, o, seed=5):
     rng = np.random.default_rng(seed)
     ids = rng.choice(w.m, size=1024, replace=False)
-    _, to = o.leaf_offsets()
-    counts = np.diff(to)
-    heavy = int(np.argmax(counts))
-    _, tperm = o.perm()
-    heavy_ids = tperm[to[heavy]:to[heavy + 1]]
-    return np.unique(np.concatenate([ids, heavy_ids]).astype(np.int64))
+    return np.unique(np.concatenate([ids, heavy_leaf_ids(o)]).astype(np.int64))
 
 
 @pytest.mark.parametrize("name", FULL)
@@ -95,7 +98,13 @@ def test_fullsize_within_paper_bound_of_direct_sum(cache, name):
     import oracle
 
     w, d, g, o, phi = setup(cache, name)
-    ids = sample_ids(w, o)[:48]
+    # 24 seeded targets plus up to 24 targets of the most loaded leaf (the direct sums over all
+    # 16.8M sources are the slow part of this test)
+    rng = np.random.default_rng(7)
+    heavy = heavy_leaf_ids(o)
+    ids = np.unique(np.concatenate([rng.choice(w.m, size=24, replace=False),
+                                    heavy[np.linspace(0, len(heavy) - 1, min(24, len(heavy))).astype(int)]]))
+    assert np.isin(heavy[0], ids) and np.isin(heavy[-1], ids)
     direct = oracle.direct(d["src_xy"], d["u"], d["tgt_xy"], w.self_mode, ids)
     bound = o.bound(ids)
     assert np.all(np.abs(phi[ids].real - direct.real) <= bound)

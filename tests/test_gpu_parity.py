@@ -237,3 +237,20 @@ def test_direct_sum_coincident_raises():
     with pytest.raises(FmmError) as e:
         direct(src, np.ones(2), tgt, out=np.zeros(2, np.complex128))
     assert e.value.code == 3
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_locals_per_level(pair_cache, name):
+    """the local expansions b_0..b_p of every evaluated cell (cells with targets), level by
+    level, against the oracle's L2L + M2L (App. B.4/B.5; D15 normwise per level) -- M2L and L2L
+    checked directly, not only through the potentials"""
+    from paper_1204_3105_b200 import X
+
+    w, d, g, o, _ = pair(pair_cache, name)
+    rng = np.random.default_rng(11)
+    for l in range(1, w.depth + 1):
+        owners = g.export(X.E4_OWNERS, l)  # cells of level l with targets
+        gl = g.export(X.LOCAL, l).reshape(-1, w.p + 1)
+        cells = owners if len(owners) <= 1500 else np.sort(rng.choice(owners, 1500, replace=False))
+        ref = np.array([o.local(l, int(c)) for c in cells])
+        assert normwise(gl[cells], ref) <= TOL, l
