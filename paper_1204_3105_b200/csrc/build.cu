@@ -40,9 +40,9 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 p = xy[i];
-  if (u) {
+  if (rec) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
     rec[2 * i] = p;
-    rec[2 * i + 1] = make_double2(u[i], 0.0);
+    rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
   }
   uint32_t k;
   if (!geo_key(g, p.x, p.y, &k)) {
@@ -162,15 +162,16 @@ __device__ __forceinline__ unsigned radix_peers(unsigned d, int db, bool valid) 
   return peers;
 }
 
+template <int SEG = RS_SEG>
 __global__ void __launch_bounds__(RS_T) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                           int db, int32_t* __restrict__ tile_hist, int ntiles) {
   __shared__ int cnt[RS_W][1 << RS_MAXB];
   const int nb = 1 << db, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int d = lane; d < nb; d += 32) cnt[w][d] = 0;
   __syncwarp();
-  const int64_t seg0 = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * RS_SEG;
+  const int64_t seg0 = (int64_t)blockIdx.x * (RS_W * SEG) + (int64_t)w * SEG;
   const unsigned mask = (unsigned)nb - 1u;
-  for (int r = 0; r < RS_SEG / 32; ++r) {
+  for (int r = 0; r < SEG / 32; ++r) {
     const int64_t i = seg0 + 32 * r + lane;
     const bool valid = i < n;
     const unsigned d = valid ? ((keys[i] >> shift) & mask) : 0u;
@@ -238,16 +239,156 @@ __global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __rest
   }
 }
 
-// ------------------------------------------------------------------ gathers
-__global__ void k_gather_src(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ rec,
-                             double2* __restrict__ sxy, double* __restrict__ su) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t j = perm[i];
-  const double2 v = rec[2 * j], w = rec[2 * j + 1];  // one 32-byte sector
-  sxy[i] = make_double2(__dadd_rn(v.x, 0.0), __dadd_rn(v.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
-  su[i] = w.x;
+// tile digit counts of the record sort: all of a thread's keys loaded first (one memory latency
+// per tile), counted with shared-memory atomics (the counts do not depend on order)
+__global__ void __launch_bounds__(RS_T) k_radix_count(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                                        int db, int32_t* __restrict__ tile_hist, int ntiles,
+                                                        int tile_elems) {
+  __shared__ int cnt[1 << RS_MAXB];
+  const int nb = 1 << db;
+  const unsigned mask = (unsigned)nb - 1u;
+  for (int d = threadIdx.x; d < nb; d += RS_T) cnt[d] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * tile_elems;
+  const int64_t t1 = min(n, t0 + tile_elems);
+  for (int64_t i = t0 + threadIdx.x; i < t1; i += RS_T) atomicAdd(&cnt[(keys[i] >> shift) & mask], 1);
+  __syncthreads();
+  for (int d = threadIdx.x; d < nb; d += RS_T) tile_hist[(int64_t)d * ntiles + blockIdx.x] = cnt[d];
 }
+
+// The same stable scatter carrying the 32-byte record (x, y, u, input index) of each key
+// instead of an index, so that the sorted sources come out of the last pass in place (no random
+// gather after the sort), staged through shared memory: a tile of RR_TILE elements is first
+// placed in digit order in shared memory (tile-local offsets of the digits + the stable rank),
+// then written out by consecutive threads, so that the elements of one digit -- consecutive
+// output positions -- leave in coalesced runs instead of one 16-byte store per element.
+// FINAL: the last pass writes the record's fields to their SoA homes (sorted positions with a
+// canonical +0 for a -0 coordinate, D13; strengths when su != NULL; the permutation) and the
+// sorted keys (for the leaf CSR).
+constexpr int RR_SEG = 256, RR_TILE = RS_W * RR_SEG;
+constexpr size_t RR_SMEM = sizeof(int) * (RS_W + 2) * (1 << RS_MAXB) + sizeof(uint32_t) * RR_TILE +
+                           2 * sizeof(double2) * RR_TILE;
+template <bool FINAL>
+__global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __restrict__ keys,
+                                                              const double2* __restrict__ rec, int64_t n, int shift,
+                                                              int db, const int32_t* __restrict__ tile_off,
+                                                              int ntiles, uint32_t* __restrict__ keys_out,
+                                                              double2* __restrict__ rec_out,
+                                                              double2* __restrict__ sxy, double* __restrict__ su,
+                                                              int32_t* __restrict__ perm) {
+  extern __shared__ double2 rr_smem[];
+  double2* srec = rr_smem;                                   // [RR_TILE][2]
+  uint32_t* skey = (uint32_t*)(srec + 2 * RR_TILE);          // [RR_TILE]
+  int* wb = (int*)(skey + RR_TILE);                          // [RS_W][1 << RS_MAXB]
+  int* loff = wb + RS_W * (1 << RS_MAXB);                    // tile-local digit starts
+  int* goff = loff + (1 << RS_MAXB);                         // global - local offset per digit
+  __shared__ int s_wsum[RS_W];
+  const int nb = 1 << db, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned mask = (unsigned)nb - 1u, lt = (1u << lane) - 1u;
+  for (int d = lane; d < nb; d += 32) wb[w * (1 << RS_MAXB) + d] = 0;
+  __syncwarp();
+  const int64_t tile0 = (int64_t)blockIdx.x * RR_TILE;
+  const int64_t seg0 = tile0 + (int64_t)w * RR_SEG;
+  // 0. every key and record of the warp's segment into registers at once (one memory latency
+  // per tile instead of one per round)
+  constexpr int NR = RR_SEG / 32;
+  uint32_t kr[NR];
+  double2 ra[NR], rb[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int64_t i = seg0 + 32 * r + lane;
+    kr[r] = i < n ? keys[i] : 0u;
+    ra[r] = i < n ? rec[2 * i] : make_double2(0.0, 0.0);
+    rb[r] = i < n ? rec[2 * i + 1] : make_double2(0.0, 0.0);
+  }
+  // 1. per-warp digit counts
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const bool valid = seg0 + 32 * r + lane < n;
+    const unsigned d = valid ? ((kr[r] >> shift) & mask) : 0u;
+    const unsigned peers = radix_peers(d, db, valid);
+    if (valid && lane == __ffs(peers) - 1) wb[w * (1 << RS_MAXB) + d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // 2. per digit: each warp's rank base within the digit, and the tile count (into loff)
+  for (int d = threadIdx.x; d < nb; d += RS_T) {
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < RS_W; ++q) {
+      const int c = wb[q * (1 << RS_MAXB) + d];
+      wb[q * (1 << RS_MAXB) + d] = run;
+      run += c;
+    }
+    loff[d] = run;
+  }
+  __syncthreads();
+  // exclusive scan of the tile counts over the digits (RS_T threads x nb / RS_T digits)
+  {
+    const int per = (nb + RS_T - 1) / RS_T, d0 = threadIdx.x * per;
+    int v[4], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = (k < per && d0 + k < nb) ? loff[d0 + k] : 0;
+      sum += v[k];
+    }
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[w] = x;
+    __syncthreads();
+    int base = 0;
+    for (int q = 0; q < w; ++q) base += s_wsum[q];
+    int run = base + x - sum;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < per && d0 + k < nb) {
+        loff[d0 + k] = run;
+        goff[d0 + k] = tile_off[(int64_t)(d0 + k) * ntiles + blockIdx.x] - run;
+        run += v[k];
+      }
+  }
+  __syncthreads();
+  // 3. stage every element at its tile-local sorted position
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const bool valid = seg0 + 32 * r + lane < n;
+    const unsigned d = valid ? ((kr[r] >> shift) & mask) : 0u;
+    const unsigned peers = radix_peers(d, db, valid);
+    int loc = 0;
+    if (valid) loc = loff[d] + wb[w * (1 << RS_MAXB) + d] + __popc(peers & lt);
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wb[w * (1 << RS_MAXB) + d] += __popc(peers);
+    if (valid) {
+      skey[loc] = kr[r];
+      srec[2 * loc] = ra[r];
+      srec[2 * loc + 1] = rb[r];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // 4. write out in tile-sorted order: runs of one digit go to consecutive positions
+  const int cnt = (int)min((int64_t)RR_TILE, n - tile0);
+  for (int j = threadIdx.x; j < cnt; j += RS_T) {
+    const uint32_t k = skey[j];
+    const int64_t g = goff[(k >> shift) & mask] + j;
+    const double2 a = srec[2 * j], b = srec[2 * j + 1];
+    keys_out[g] = k;
+    if (FINAL) {
+      sxy[g] = make_double2(__dadd_rn(a.x, 0.0), __dadd_rn(a.y, 0.0));  // -0 -> +0 (D13, p2p.cu)
+      if (su) su[g] = b.x;
+      perm[g] = (int32_t)__double_as_longlong(b.y);
+    } else {
+      rec_out[2 * g] = a;
+      rec_out[2 * g + 1] = b;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gathers
 // multi-rank: the kept sources gathered straight from the caller's arrays (no packed record:
 // the rank keeps ~1/R of the points, so writing a record for every point would cost more)
 __global__ void k_gather_src_in(const int32_t* __restrict__ perm, int64_t n, const double2* __restrict__ xy,
@@ -660,6 +801,81 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
 // leaves, and the stable compaction of the points it keeps (a second host sync reads their
 // counts).  ckey / cidx (n + m entries each) receive the kept keys and input indices: sources
 // first, then targets (distinct-target trees).
+// stable LSD radix sort of (key, 32-byte record) pairs of one rank's points: the records move
+// with the keys through every pass and the last pass writes the sorted SoA arrays and the
+// permutation; then the leaf CSR off[0..K+1] from the sorted keys
+static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2* rec, int64_t n, double2* xy_out,
+                              double* u_out, int32_t* perm, int32_t* off) {
+  cudaStream_t s = t->stream;
+  if (n == 0) {
+    FMM_CUDA_TRY(cudaMemsetAsync(off, 0, sizeof(int32_t) * (t->g.K + 2), s));
+    return FMM_OK;
+  }
+  const int bits = key_bits(t->g.K);
+  const int passes = (bits + RS_MAXB - 1) / RS_MAXB;
+  const int ntiles = (int)((n + RR_TILE - 1) / RR_TILE);
+  const int64_t nhist = ((int64_t)1 << ((bits + passes - 1) / passes)) * ntiles;
+  static bool attr_set = false;
+  if (!attr_set) {
+    FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)RR_SMEM));
+    FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)RR_SMEM));
+    attr_set = true;
+  }
+  // scratch: kA kB (n u32), record ping-pong (n x 32 B each: one buffer for two passes, two for
+  // more), hist, scan scratch
+  const int nrec = passes > 2 ? 2 : (passes > 1 ? 1 : 0);
+  const size_t rec_bytes = (size_t)n * 32;
+  const size_t need = 256 + (size_t)n * 8 + 256 + nrec * (rec_bytes + 256) + (size_t)nhist * 4 +
+                      fmm_scan_scratch_bytes(nhist) + 256;
+  if (t->scratch_bytes < need) {
+    if (t->scratch) cudaFreeAsync(t->scratch, s);
+    t->scratch = nullptr;
+    FMM_CUDA_TRY(cudaMallocAsync(&t->scratch, need, s));
+    t->scratch_bytes = need;
+  }
+  char* p = (char*)t->scratch;
+  auto take = [&](size_t b) {
+    char* q = p;
+    p += (b + 255) & ~(size_t)255;
+    return q;
+  };
+  uint32_t* kA = (uint32_t*)take((size_t)n * 4);
+  uint32_t* kB = (uint32_t*)take((size_t)n * 4);
+  double2* rA = nrec > 0 ? (double2*)take(rec_bytes) : nullptr;
+  double2* rB = nrec > 1 ? (double2*)take(rec_bytes) : nullptr;
+  int32_t* hist = (int32_t*)take((size_t)nhist * 4);
+  void* sscr = p;
+  const uint32_t* kin = keys;
+  const double2* rin = rec;
+  int shift = 0;
+  for (int ps = 0; ps < passes; ++ps) {
+    const int db = bits / passes + (ps < bits % passes ? 1 : 0);
+    const int64_t nh = ((int64_t)1 << db) * ntiles;
+    uint32_t* kout = (ps % 2 == 0) ? kA : kB;
+    double2* rout = (ps % 2 == 0) ? rA : rB;
+    k_radix_count<<<ntiles, RS_T, 0, s>>>(kin, n, shift, db, hist, ntiles, RR_TILE);
+    int e = fmm_device_scan_i32(hist, hist, nh, sscr, fmm_scan_scratch_bytes(nh), s, &t->launches);
+    if (e) return e;
+    if (ps == passes - 1)
+      k_radix_scatter_rec<true><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, nullptr,
+                                                              xy_out, u_out, perm);
+    else
+      k_radix_scatter_rec<false><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, rout,
+                                                               nullptr, nullptr, nullptr);
+    t->launches += 2;
+    FMM_CUDA_TRY(cudaGetLastError());
+    kin = kout;
+    rin = rout;
+    shift += db;
+  }
+  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
+  return FMM_OK;
+}
+
 static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64_t* dcount) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
@@ -731,7 +947,10 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
   const Geo& G = t->g;
   DGeo g = dgeo(G);
   const bool multi = t->cfg.nranks > 1;
-  double2* rec = nullptr;  // (x, y, u, 0) per source, input order (one rank only)
+  // one rank: (x, y, u, index) records of sources (and of distinct targets) that the radix sort
+  // carries to their sorted positions
+  double2* rec = nullptr;
+  double2* trec = nullptr;
   if (multi) {
     FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (G.K + 2), s));
     if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (G.K + 2), s));
@@ -743,8 +962,9 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
     t->launches++;
   }
   if (!G.self_mode && t->m > 0) {
+    if (!multi) FMM_CUDA_TRY(cudaMallocAsync((void**)&trec, (size_t)t->m * 32, s));
     k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->status,
-                                                  nullptr, nullptr, multi ? t->gtoff : nullptr);
+                                                  nullptr, trec, multi ? t->gtoff : nullptr);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
@@ -765,27 +985,24 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
     e = multi_rank_select(t, ckey, cidx, dcount);
   }
   if (t->timing) cudaEventRecord(t->ev[9], s);
-  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain kept points)
+  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain kept points).
+  // One rank: the records travel with the keys.  Multi-rank: the compacted (key, input index)
+  // pairs are sorted and the kept points gathered from the caller's arrays.
   if (!e) e = multi ? radix_sort_perm(t, ckey, t->n_loc, t->sperm, t->soff, cidx)
-                    : radix_sort_perm(t, t->skey, t->n, t->sperm, t->soff);
+                    : radix_sort_records(t, t->skey, rec, t->n, t->sxy, t->su, t->sperm, t->soff);
   if (!e && !G.self_mode)
     e = multi ? radix_sort_perm(t, ckey + t->n, t->m_loc, t->tperm, t->toff, cidx + t->n)
-              : radix_sort_perm(t, t->tkey, t->m, t->tperm, t->toff);
+              : radix_sort_records(t, t->tkey, trec, t->m, t->txy, nullptr, t->tperm, t->toff);
   if (ckey) cudaFreeAsync(ckey, s);
-  if (e) {
-    if (rec) cudaFreeAsync(rec, s);
-    return e;
-  }
-  if (t->n_loc > 0) {
-    if (multi)
-      k_gather_src_in<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, (const double2*)t->src_xy_in,
-                                                                 t->src_u_in, t->sxy, t->su);
-    else
-      k_gather_src<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, rec, t->sxy, t->su);
+  if (rec) cudaFreeAsync(rec, s);
+  if (trec) cudaFreeAsync(trec, s);
+  if (e) return e;
+  if (multi && t->n_loc > 0) {
+    k_gather_src_in<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, (const double2*)t->src_xy_in,
+                                                               t->src_u_in, t->sxy, t->su);
     t->launches++;
   }
-  if (rec) cudaFreeAsync(rec, s);
-  if (!G.self_mode && t->m_loc > 0) {
+  if (multi && !G.self_mode && t->m_loc > 0) {
     k_gather_xy<<<blocks_for(t->m_loc, 256), 256, 0, s>>>(t->tperm, t->m_loc, (const double2*)t->tgt_xy_in, t->txy);
     t->launches++;
   }
