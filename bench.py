@@ -181,7 +181,9 @@ def run_gpu(args):
 
     def one_step(timing=False, host=False, pipelined=False, fork=True, join=True, parity=0, kept=None):
         """one build + evaluate per tiling; every tree releases its device memory stream-ordered
-        at the end of its own evaluation, so one tree's memory is live at a time"""
+        at the end of its own evaluation, so one tree's memory is live at a time (one stream).
+        pipelined: one stream per tiling, forked from the timed stream at the step's start and
+        joined at its end (when fork / join)."""
         launches = 0
         streams = side[parity] if pipelined else {nm: stream for nm in names}
         for nm in names:
@@ -263,16 +265,19 @@ def run_gpu(args):
     total_targets = sum(inputs[nm][0].m for nm in names) * args.steps
 
     # ---- e2e: same metric through the C ABI with pinned host buffers (H2D + D2H inside)
-    def e2e_run(pipelined):
-        one_step(host=True, pipelined=pipelined)
+    def e2e_run(mode):
+        """serial: one stream; step: one stream per tiling forked and joined every step, so one
+        tiling's copies overlap another tiling's kernels inside the step; cross: the streams
+        alternate by step and join only at the end (copies also overlap the previous step)"""
+        one_step(host=True, pipelined=mode != "serial")
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for s_ in range(args.steps):
-            if pipelined:  # a tiling's next copy waits only for its own previous step
+            if mode == "cross":  # a tiling's next copy waits only for its own previous step
                 one_step(host=True, pipelined=True, fork=(s_ < 2), join=(s_ >= args.steps - 2), parity=s_ % 2)
             else:
-                one_step(host=True)
+                one_step(host=True, pipelined=mode == "step")
         f1.record(stream)
         barrier()
         t_ = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
@@ -280,8 +285,9 @@ def run_gpu(args):
             dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         return float(t_.item())
 
-    e2e_ms = e2e_run(False)
-    e2e_pipe_ms = e2e_run(True) if args.e2e_pipelined else None
+    e2e_mode = "step" if len(names) > 1 else "serial"
+    e2e_ms = e2e_run(e2e_mode)
+    e2e_pipe_ms = e2e_run("cross") if args.e2e_pipelined else None
     h2d = sum(w.n * 24 + (0 if w.self_mode else w.m * 16) for w, _ in inputs.values())
     d2h = sum(w.m * 16 for w, _ in inputs.values())
 
@@ -331,22 +337,26 @@ def run_gpu(args):
         "data": "synthetic, seeded numpy PCG64 (fmm_inputs), shapes of BASELINE.json configs",
         "config": {"workload": args.workload + ": " + "; ".join(inputs[nm][0].note for nm in names),
                    "tilings": names, "step": "fmm_build_tree + fmm_evaluate per tiling",
-                   "streams": "timed region and e2e: one stream, steps serial",
+                   "streams": "timed region: one stream, steps serial",
                    "memory": "each tree is released stream-ordered after its evaluation (one tree live at a time)",
                    "l2": "inputs larger than L2 (>= 400 MB per tiling)", "per_tiling": per_tiling},
         "roofline": roof,
         "roofline_m2l": roof_m2l,
         "e2e": {"value": total_targets / (e2e_ms / 1e3), "unit": "target evals/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
-                "how": "fmm_build_tree from pinned host inputs + fmm_evaluate into a pinned host output, "
-                       "serial on the timed stream (copies inside the timed region)"},
+                "how": "every step: fmm_build_tree from pinned host inputs + fmm_evaluate into a pinned host "
+                       "output per tiling (H2D / D2H copies inside the timed region), "
+                       + ("one CUDA stream per tiling, forked from the timed stream at the start of each step "
+                          "and joined at its end: one tiling's copies overlap another tiling's kernels inside "
+                          "the step, nothing overlaps across steps" if e2e_mode == "step" else
+                          "serial on the timed stream")},
         "gpu_launches": launches,
         "clocks": clk,
     }
     if e2e_pipe_ms is not None:
         res["e2e_pipelined"] = {"value": total_targets / (e2e_pipe_ms / 1e3), "unit": "target evals/s",
-                                "how": "two CUDA streams per tiling alternating by step: a step's copies overlap "
-                                       "other steps' kernels (not comparable with the serial device-timed value)"}
+                                "how": "two CUDA streams per tiling alternating by step, joined only at the end: "
+                                       "a step's copies also overlap the previous step's kernels"}
     if not args.no_cpu_baseline and world == 1:
         res["cpu_baseline"] = cpu_baseline(args, names, sample_targets=args.cpu_sample)
     if world > 1:
