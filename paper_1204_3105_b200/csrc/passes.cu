@@ -505,10 +505,28 @@ static void launch_down(fmm_tree_s* t, int l) {
       t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->loc + G.lvl_off[l] * (p + 1));
 }
 
+// m2l_dense.cu (NEXT-3): per-offset operators on DMMA, quadtree, FMM_M2L_DENSE=1
+bool fmm_m2l_dense_enabled(const fmm_tree_s* t);
+int fmm_m2l_dense_lmin(int L);
+int fmm_m2l_dense_level(fmm_tree_s* t, int l, int64_t c0, int64_t c1, double* Tfrag);
+size_t fmm_m2l_dense_table_bytes(int p);
+
 int fmm_stage_downward(fmm_tree_s* t) {
   const Geo& G = t->g;
   const int p = G.p;
+  double* Tfrag = nullptr;
+  const int ldense = fmm_m2l_dense_enabled(t) ? fmm_m2l_dense_lmin(G.L) : G.L + 1;
+  if (ldense <= G.L) FMM_CUDA_TRY(cudaMallocAsync((void**)&Tfrag, fmm_m2l_dense_table_bytes(p), t->stream));
   for (int l = 1; l <= G.L; ++l) {
+    if (l >= ldense) {
+      int64_t c0, c1;
+      level_range(t, l, &c0, &c1);
+      if (c1 > c0) {
+        int e = fmm_m2l_dense_level(t, l, c0, c1, Tfrag);
+        if (e) return e;
+      }
+      continue;
+    }
     if (p <= 8) launch_down<8>(t, l);
     else if (p <= 12) launch_down<12>(t, l);
     else if (p <= 16) launch_down<16>(t, l);
@@ -518,6 +536,7 @@ int fmm_stage_downward(fmm_tree_s* t) {
     else launch_down<32>(t, l);
     t->launches++;
   }
+  if (Tfrag) cudaFreeAsync(Tfrag, t->stream);
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
