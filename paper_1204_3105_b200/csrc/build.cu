@@ -562,24 +562,12 @@ __global__ void k_halo_flags(int64_t lo, int64_t hi, const int32_t* __restrict__
   for (int q = 0; q < nnear[t]; ++q) flag[near[t * FMM_NEAR_MAX + q]] = 1;
 }
 
-// every leaf t in [0, K): pack the keep flags into the bitmask (one word per warp), and give the
-// halo leaves outside [lo, hi) their near lists (the P2P tasks of symmetric blocks start from
-// the smaller leaf, which may be a halo leaf); leaves neither own nor halo get empty lists
-__global__ void __launch_bounds__(256) k_near_halo(DGeo g, int64_t K, int64_t lo, int64_t hi,
-                                                   const int32_t* __restrict__ gsoff,
-                                                   const int32_t* __restrict__ gtoff,
-                                                   const uint8_t* __restrict__ flag, int32_t* __restrict__ near,
-                                                   int32_t* __restrict__ nnear, uint32_t* __restrict__ bits) {
+// the keep flags (bytes) packed into the leaf bitmask, one word per warp
+__global__ void __launch_bounds__(256) k_pack_bits(int64_t K, const uint8_t* __restrict__ flag,
+                                                   uint32_t* __restrict__ bits) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool f = t <= K && flag[t];
-  const unsigned word = __ballot_sync(0xffffffffu, f);
+  const unsigned word = __ballot_sync(0xffffffffu, t <= K && flag[t]);
   if ((threadIdx.x & 31) == 0 && t <= K) bits[t >> 5] = word;
-  if (t >= K || (t >= lo && t < hi)) return;
-  if (!f || gtoff[t + 1] == gtoff[t]) {
-    nnear[t] = 0;
-    return;
-  }
-  near_of(g, t, gsoff, near, nnear);
 }
 
 // Stable single-pass compaction of the kept points (input order, so that the sort by key then
@@ -893,8 +881,8 @@ static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64
   // near lists (global emptiness) and the partition
   e = fmm_stage_near_partition(t);
   if (e) return e;
-  // halo flags of the source leaves (bytes, then a bitmask with the halo near lists), then
-  // stable compactions of the kept points
+  // halo flags of the source leaves (bytes, then a bitmask), then stable compactions of the kept
+  // points
   const int64_t nwords = (K + 1 + 31) / 32;
   uint32_t* bits = (uint32_t*)t->lflag;
   uint8_t* flag8 = (uint8_t*)(bits + nwords);
@@ -902,8 +890,7 @@ static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64
   if (t->leaf_hi > t->leaf_lo)
     k_halo_flags<<<blocks_for(t->leaf_hi - t->leaf_lo, 128), 128, 0, s>>>(t->leaf_lo, t->leaf_hi, t->gtoff,
                                                                           t->near, t->nnear, flag8);
-  k_near_halo<<<blocks_for(K + 1, 256), 256, 0, s>>>(dgeo(G), K, t->leaf_lo, t->leaf_hi, t->gsoff, t->gtoff, flag8,
-                                                     t->near, t->nnear, bits);
+  k_pack_bits<<<blocks_for(K + 1, 256), 256, 0, s>>>(K, flag8, bits);
   t->launches += 2;
   // the bitmask goes to shared memory when it fits (<= 160 KB: 1.3M leaves)
   const int smem_words = nwords * 4 <= 160 * 1024 ? (int)nwords : 0;
@@ -1013,66 +1000,59 @@ int fmm_stage_keys_sort(fmm_tree_s* t) {
 namespace {
 // estimated evaluation work of each leaf (P2P pairs + per-target L2P + per-leaf downward),
 // summed over blocks of FMM_PART_BLOCK leaves (the multi-rank partition)
-// The estimate uses the leaf's own counts: w_t = n_t^tgt * (n_t^src * P2) + 2 (p+1) n_t^tgt +
-// 40 (p+1)^2, i.e. the near field as if every near leaf held as many sources as t (exact
-// for uniform trees up to the boundary; the partition only needs a balance estimate, and it
-// then needs no near list of any leaf outside the rank's range and halo).
-__global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff, int p2,
-                             int p, double* __restrict__ bw) {
-  __shared__ double warp_sum[FMM_PART_BLOCK / 32];
-  int64_t leaf = blockIdx.x * (int64_t)FMM_PART_BLOCK + threadIdx.x;
+// Work estimate of leaf t: w_t = n_t^tgt * sum_{s in near(t)} n_s^src (its near-field pairs)
+// + 2 (p+1) n_t^tgt (L2P) + 40 (p+1)^2 (its M2L), from the global counts and the near lists of
+// every leaf; summed per block of FMM_PART_BLOCK (= 32, one warp) leaves.  Clustered inputs
+// need both: a few dense leaves carry a large share of the work, and their neighbours' counts
+// differ from their own.
+__global__ void k_block_work(int64_t K, const int32_t* __restrict__ soff, const int32_t* __restrict__ toff,
+                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int p,
+                             double* __restrict__ bw) {
+  const int64_t leaf = blockIdx.x * (int64_t)FMM_PART_BLOCK + threadIdx.x;
   double w = 0.0;
   if (leaf < K) {
     const int nt = toff[leaf + 1] - toff[leaf];
     if (nt > 0) {
-      const int ns = soff[leaf + 1] - soff[leaf];
-      w = (double)nt * (double)ns * p2 + 2.0 * (p + 1) * nt + 40.0 * (p + 1) * (p + 1);
+      int64_t ns = 0;
+      for (int q = 0; q < nnear[leaf]; ++q) {
+        const int sl = near[leaf * FMM_NEAR_MAX + q];
+        ns += soff[sl + 1] - soff[sl];
+      }
+      w = (double)nt * (double)ns + 2.0 * (p + 1) * nt + 40.0 * (p + 1) * (p + 1);
     }
   }
+  static_assert(FMM_PART_BLOCK == 32, "one warp per work block");
   for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = w;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < FMM_PART_BLOCK / 32; ++i) s += warp_sum[i];
-    bw[blockIdx.x] = s;
-  }
+  if (threadIdx.x == 0) bw[blockIdx.x] = w;
 }
+
 }  // namespace
 
-// one rank: near lists of every leaf.  nranks > 1: the work-balanced leaf range of this rank
-// (one host sync), then the near lists of its own leaves
+// near lists of every leaf (global emptiness); nranks > 1: then the work-balanced leaf range of
+// this rank (one host sync)
 int fmm_stage_near_partition(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
+  k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear, 0, G.K);
+  t->launches++;
+  FMM_CUDA_TRY(cudaGetLastError());
   if (t->cfg.nranks <= 1) {
     t->leaf_lo = 0;
     t->leaf_hi = G.K;
-    k_near<<<blocks_for(G.K, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear, 0, G.K);
-    t->launches++;
-    FMM_CUDA_TRY(cudaGetLastError());
     return FMM_OK;
   }
   int64_t nb = (G.K + FMM_PART_BLOCK - 1) / FMM_PART_BLOCK;
   double* bw = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync((void**)&bw, nb * sizeof(double), s));
-  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->gsoff, t->gtoff, G.nslot, G.p, bw);
+  k_block_work<<<(unsigned)nb, FMM_PART_BLOCK, 0, s>>>(G.K, t->gsoff, t->gtoff, t->near, t->nnear, G.p, bw);
   t->launches++;
   std::vector<double> hb(nb);
   cudaError_t ce = cudaMemcpyAsync(hb.data(), bw, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
   cudaFreeAsync(bw, s);
   FMM_CUDA_TRY(ce);
-  int e = fmm_partition(hb.data(), nb, FMM_PART_BLOCK, G.K, t->cfg.rank, t->cfg.nranks, &t->leaf_lo, &t->leaf_hi);
-  if (e) return e;
-  if (t->leaf_hi > t->leaf_lo) {
-    k_near<<<blocks_for(t->leaf_hi - t->leaf_lo, 128), 128, 0, s>>>(g, t->gsoff, t->gtoff, t->near, t->nnear,
-                                                                   t->leaf_lo, t->leaf_hi);
-    t->launches++;
-  }
-  FMM_CUDA_TRY(cudaGetLastError());
-  return FMM_OK;
+  return fmm_partition(hb.data(), nb, FMM_PART_BLOCK, G.K, t->cfg.rank, t->cfg.nranks, &t->leaf_lo, &t->leaf_hi);
 }
 
 int fmm_stage_tables_lists(fmm_tree_s* t) {

@@ -13,7 +13,7 @@
 #define FMM_MAX_P 32
 #define FMM_CAND_MAX 64  // >= 4*13 (triangle), 7*7 (septree), 4*9 (quad) E4 candidates per sibling group
 #define FMM_NEAR_MAX 16  // >= 13 (triangle near set incl. self)
-#define FMM_PART_BLOCK 256  // leaves per work block of the multi-rank partition
+#define FMM_PART_BLOCK 32  // leaves per work block of the multi-rank partition (one warp)
 
 // ---------------------------------------------------------------- host-side geometry constants
 struct Geo {

@@ -85,7 +85,7 @@ def test_partition_tiles_leaf_range(world, kind):
 # ---------------------------------------------------------------- the multipole exchange (gloo)
 def _exchange_worker(rank, world, port, name, q):
     """rank r: its work-balanced leaf range (the library's fmm_partition on the block-work
-    estimate of the multi-rank build), P2M over its own source leaves and M2M of those partial
+    estimate), P2M over its own source leaves and M2M of those partial
     expansions up every level (oracle operators, App. B.2/B.3), all other cells zero; the
     per-level multipole trees are then summed over the ranks with a gloo all_reduce -- the
     exchange fmm_evaluate does with ncclAllReduce.  Rank 0 reports the summed
@@ -106,7 +106,7 @@ def _exchange_worker(rank, world, port, name, q):
     K = B ** w.depth
     so, to = T.leaf_offsets()
     ns, nt = np.diff(so), np.diff(to)
-    # block work of the multi-rank build (build.cu k_block_work): n_t (n_s P2) + 2 (p+1) n_t + 40 (p+1)^2
+    # a block-work estimate over 256-leaf blocks (the build uses near-list sums per 32-leaf block)
     P2 = {"quad": 9, "sept": 7, "triq": 13}[w.tiling]
     lw = np.where(nt > 0, nt * ns * float(P2) + 2.0 * (w.p + 1) * nt + 40.0 * (w.p + 1) ** 2, 0.0)
     nb = (K + 255) // 256
