@@ -98,35 +98,68 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 }
 
 // ------------------------------------------------------------------ M2M (one warp per parent, lane = coefficient)
-// a child's multipole is staged once in shared memory (one coalesced load), so that the
-// Horner loop of lane k reads a_j without a memory round trip per step
-__global__ void __launch_bounds__(128) k_m2m(int B, int64_t par0, int64_t nparents, int64_t span_l,
+// All B children's multipoles (and the binomial rows) are staged in shared memory first, with
+// one load latency for all of them, and lane k then runs the B children's Horner chains in
+// step (B independent chains: the latency of one is hidden by the others); the children are
+// added in ascending order as before.
+template <int B>
+__global__ void __launch_bounds__(128) k_m2m(int64_t par0, int64_t nparents, int64_t span_l,
                                              const int32_t* __restrict__ soff,
                                              const double2* __restrict__ cen_par, const double2* __restrict__ cen_ch,
                                              const double2* __restrict__ mp_ch, int p, const double* __restrict__ binom,
                                              double2* __restrict__ mp_par) {
-  __shared__ double2 s_a[4][32];
-  const int64_t P = par0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // parents [par0, nparents)
+  __shared__ double2 s_a[4][B][32];
+  __shared__ double2 s_z[4][B];   // c_child - c_parent of the staged children
+  __shared__ double s_c[32][33];  // s_c[k][j] = C(k - 1, j - 1)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+    const int k = i >> 5, j = i & 31;
+    s_c[k][j] = (k >= 1 && j >= 1 && j <= k) ? binom[(k - 1) * BS + (j - 1)] : 0.0;
+  }
+  __syncthreads();
+  const int64_t P = par0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // parents [par0, nparents)
   if (P >= nparents) return;
   const double2 cp = cen_par[P];
   const int k = lane;  // p <= 31: one coefficient per lane
-  double2 acc = make_double2(0.0, 0.0);
+  // non-empty children, in ascending order, staged at the front of s_a (empty children add
+  // nothing: clustered trees have many)
+  int nc = 0;
+#pragma unroll
   for (int ch = 0; ch < B; ++ch) {
     const int64_t c = P * B + ch;
     if (soff[(c + 1) * span_l] == soff[c * span_l]) continue;
-    __syncwarp();
-    s_a[w][lane] = lane <= p ? mp_ch[c * (p + 1) + lane] : make_double2(0.0, 0.0);
-    __syncwarp();
-    const double Q = s_a[w][0].x;
-    if (k == 0) {
-      acc.x += Q;
-    } else if (k <= p) {
+    s_a[w][nc][lane] = lane <= p ? mp_ch[c * (p + 1) + lane] : make_double2(0.0, 0.0);
+    if (lane == 0) {
       const double2 cc = cen_ch[c];
-      const double2 z0 = make_double2(cc.x - cp.x, cc.y - cp.y);
-      double2 h = make_double2(-Q / k, 0.0);
-      for (int j = 1; j <= k; ++j) h = cadd(cmul(h, z0), cscale(binom[(k - 1) * BS + (j - 1)], s_a[w][j]));
-      acc = cadd(acc, h);
+      s_z[w][nc] = make_double2(cc.x - cp.x, cc.y - cp.y);
+    }
+    ++nc;
+  }
+  __syncwarp();
+  double2 acc = make_double2(0.0, 0.0);
+  if (k == 0) {
+    for (int q = 0; q < nc; ++q) acc.x += s_a[w][q][0].x;
+  } else if (k <= p) {
+    // up to 4 children's Horner chains in step (independent: their latencies overlap)
+    for (int q0 = 0; q0 < nc; q0 += 4) {
+      double2 h[4], z0[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool v = q0 + q < nc;
+        h[q] = make_double2(v ? -s_a[w][q0 + q][0].x / k : 0.0, 0.0);
+        z0[q] = v ? s_z[w][q0 + q] : make_double2(0.0, 0.0);
+      }
+      for (int j = 1; j <= k; ++j) {
+        const double cj = s_c[k][j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 a = q0 + q < nc ? s_a[w][q0 + q][j] : make_double2(0.0, 0.0);
+          h[q] = cadd(cmul(h[q], z0[q]), cscale(cj, a));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q0 + q < nc) acc = cadd(acc, h[q]);
     }
   }
   if (k <= p) mp_par[P * (p + 1) + k] = acc;
@@ -282,8 +315,9 @@ int fmm_stage_upward(fmm_tree_s* t) {
     int64_t c0, c1;
     level_range(t, l, &c0, &c1);
     if (c1 <= c0) continue;
-    k_m2m<<<(unsigned)(((c1 - c0) * 32 + 127) / 128), 128, 0, s>>>(
-        G.B, c0, c1, G.ncells[G.L - l - 1] /* B^(L-l-1) */, t->soff, t->centre + G.lvl_off[l],
+    auto m2m = G.B == 7 ? k_m2m<7> : k_m2m<4>;
+    m2m<<<(unsigned)(((c1 - c0) * 32 + 127) / 128), 128, 0, s>>>(
+        c0, c1, G.ncells[G.L - l - 1] /* B^(L-l-1) */, t->soff, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l + 1], t->mp + G.lvl_off[l + 1] * (p + 1), p, t->binom, t->mp + G.lvl_off[l] * (p + 1));
     t->launches++;
   }
