@@ -254,3 +254,39 @@ def test_locals_per_level(pair_cache, name):
         cells = owners if len(owners) <= 1500 else np.sort(rng.choice(owners, 1500, replace=False))
         ref = np.array([o.local(l, int(c)) for c in cells])
         assert normwise(gl[cells], ref) <= TOL, l
+
+
+@pytest.mark.parametrize("self_mode", [True, False])
+def test_tiny_separation_across_leaves(self_mode):
+    """Pairs closer than 1e-30 in DIFFERENT leaves (quadtree rooted at (-1/2, -1/2), so that the
+    cell boundaries x = 0 and y = 0 separate (+-1e-40, y) and (x, +-1e-41)): the pair kernel must
+    send them to its exact path (p2p.cu p2p_slow) in off-diagonal blocks too, where no pair is
+    excluded.  Against the oracle within the D15 gate (a garbage or dropped tiny pair,
+    |u log|z|^2| ~ 180, fails it), and bitwise repeatable."""
+    import dataclasses
+
+    import torch
+
+    from paper_1204_3105_b200 import Config, Tree
+
+    w = dataclasses.replace(SMALL_CASES["C4qs"].scaled(3000, name="tiny"), root_x=-0.5, root_y=-0.5,
+                            self_mode=self_mode, depth=4)
+    rng = np.random.default_rng(7)
+    src = rng.uniform(-0.5, 0.5, (3000, 2))
+    src[:4] = [[1e-40, 0.1], [-1e-40, 0.1], [0.2, -3e-41], [0.2, 2e-41]]
+    u = rng.uniform(-1, 1, 3000)
+    tgt = None
+    if not self_mode:
+        tgt = rng.uniform(-0.5, 0.5, (2000, 2))
+        tgt[:2] = [[-2e-40, 0.1], [0.2, 1e-41]]  # within 3e-40 of sources 0, 1 and 2, 3 (across x = 0 / y = 0)
+    d = {"src_xy": src, "u": u, "tgt_xy": tgt}
+    cfg = Config.make(w.tiling, w.depth, w.p, w.root_x, w.root_y, w.root_size, self_mode)
+    g = Tree(cfg, torch.from_numpy(src).cuda(), torch.from_numpy(u).cuda(),
+             None if tgt is None else torch.from_numpy(tgt).cuda())
+    phi = g.evaluate().cpu().numpy()
+    g.check()
+    o = oracle_tree(w, d)
+    ref = o.evaluate()
+    assert normwise(phi, ref) <= TOL
+    b = g.evaluate().cpu().numpy()
+    assert np.array_equal(phi, b)
