@@ -29,6 +29,10 @@ struct Geo {
   int sept_K;             // |lattice coordinate| bound for in-domain points
 };
 
+// partial-sum slots per target of the near field: one per near leaf in self mode (symmetric
+// blocks, p2p.cu), one in total for distinct targets (one task over all near leaves)
+inline int fmm_part_slots(const Geo& g) { return g.self_mode ? g.nslot : 1; }
+
 struct DevStatus {
   unsigned long long domain_bad;      // min offending index (ULLONG_MAX = none)
   unsigned long long coincident_bad;  // min offending target index

@@ -8,11 +8,12 @@
 // block (t < s) is therefore evaluated ONCE: every pair feeds the row target
 // (u_j Log(x_i - x_j)) and, reversed, the column target (u_i Log(x_j - x_i)).  Light blocks
 // (n_t n_s <= 65,536) are one task; heavy ones are split by rows of the larger leaf.
-// Diagonal blocks are symmetric as well (schedule below; heavy ones split by rows); the
-// distinct-target configs are one-sided.  Every (target, near-leaf) pair of the near list
-// owns one partial-sum slot, and a final pass adds the slots in near-list order.  Each slot
-// is written by exactly one task, so the result is bitwise reproducible, except the slots of
-// heavy symmetric blocks, which several row-range tasks add into atomically.
+// Diagonal blocks are symmetric as well (schedule below; heavy ones split by rows).  Every
+// (target, near-leaf) pair of the near list owns one partial-sum slot, and a final pass adds
+// the slots in near-list order.  Each slot is written by exactly one task, so the result is
+// bitwise reproducible, except the slots of heavy symmetric blocks, which several row-range
+// tasks add into atomically.  Distinct targets (one-sided) take one task per target leaf over
+// the sources of all its near leaves, concatenated in near-list order, and one slot per target.
 #include <type_traits>
 
 #include "fmm_internal.cuh"
@@ -22,6 +23,7 @@ namespace {
 
 constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) block
 constexpr int P2P_S = 192;          // sources of one near leaf kept in shared memory per warp
+constexpr int P2P_SD = 320;         // distinct targets: near-list sources kept in shared memory per warp
 constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17, TF_HEAVY = 1 << 18;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
@@ -47,13 +49,21 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
       ++c;
     }
   };
+  if (!self_mode) {
+    // distinct targets: one task (row ranges of <= 65,536 pairs) over ALL near leaves of t, their
+    // sources concatenated in near-list order as the columns; one partial-sum slot per target
+    if (!t_in) return 0;
+    int tot = 0;
+    for (int q = 0; q < nn; ++q) {
+      const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
+      tot += soff[s + 1] - soff[s];
+    }
+    if (tot > 0) emit_rows(t, 0, nt, tot, 0);
+    return c;
+  }
   for (int q = 0; q < nn; ++q) {
     const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
     const int ns = soff[s + 1] - soff[s];
-    if (!self_mode) {
-      if (t_in) emit_rows(t, q, nt, ns, 0);
-      continue;
-    }
     if (s < t) continue;  // the block belongs to the smaller leaf index
     if (s == t) {  // diagonal block: symmetric (each unordered pair once) when it fits a warp
       if (t_in) {
@@ -144,6 +154,7 @@ constexpr int P2P_RS = 32;  // row stride (double2) of the reaction scratch; col
 constexpr size_t P2P_TAB_BYTES = sizeof(double2) * (P2P_LOG_N + P2P_ATAN_N);
 constexpr size_t P2P_WARP_BYTES = sizeof(double2) * (2 * P2P_S + 4 * P2P_RS) + sizeof(double) * P2P_S;
 constexpr size_t P2P_SMEM = P2P_TAB_BYTES + P2P_WARPS * P2P_WARP_BYTES;
+static_assert(24 * P2P_SD + 64 * sizeof(double2) <= P2P_WARP_BYTES, "distinct-target warp layout");
 constexpr double P2P_PAD = 1.0e30;
 
 struct PairOut {
@@ -189,8 +200,8 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
     const double2* __restrict__ sxy, const double* __restrict__ su, const int32_t* __restrict__ near,
-    const int32_t* __restrict__ tperm, const double* __restrict__ tabs, double2* __restrict__ part, int nslot,
-    int64_t lo, int64_t hi, DevStatus* st) {
+    const int32_t* __restrict__ nnear, const int32_t* __restrict__ tperm, const double* __restrict__ tabs,
+    double2* __restrict__ part, int nslot, int64_t lo, int64_t hi, DevStatus* st) {
   extern __shared__ double2 smem[];
   double2* s_log = smem;
   double2* s_atan = s_log + P2P_LOG_N;  // P2P_ATAN_N entries (garbage k of |z| < 1e-30 stays inside)
@@ -198,9 +209,11 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double2* const s_xy = (double2*)((char*)smem + P2P_TAB_BYTES + w * P2P_WARP_BYTES);  // sources of s
+  // self mode: s_xy[P2P_S], reactions s_re[P2P_S], scratch s_rs[4 P2P_RS], strengths s_u[P2P_S];
+  // distinct targets (no reactions): s_xy[P2P_SD], s_u[P2P_SD], row-sum scratch s_rs[64]
   double2* const s_re = s_xy + P2P_S;    // reactions of the sources of s (self mode)
-  double2* const s_rs = s_re + P2P_S;    // [4 row lanes][P2P_RS] reaction partials of a chunk
-  double* const s_u = (double*)(s_rs + 4 * P2P_RS);
+  double2* const s_rs = SELF ? s_re + P2P_S : (double2*)((char*)s_xy + 24 * P2P_SD);
+  double* const s_u = SELF ? (double*)(s_rs + 4 * P2P_RS) : (double*)(s_xy + P2P_SD);
   const int tl = lane & 3, ph = lane >> 2;
   const double PI = 3.141592653589793;
   const int ntask = *ntask_p;
@@ -219,13 +232,47 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     // is then counted once (tests/test_p2p_schedule.py enumerates the rule)
     const bool sd = sym && diag;
     const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
-    const int tb = toff[t], sb = soff[s], ns = soff[s + 1] - sb;
+    const int tb = toff[t];
+    // distinct targets: the columns are the sources of all near leaves of t, concatenated
+    const int nn = SELF ? 1 : nnear[t];
+    int sb = soff[s], ns = soff[s + 1] - sb;
+    if (!SELF)
+      for (int k = 1; k < nn; ++k) {
+        const int s2 = near[(int64_t)t * FMM_NEAR_MAX + k];
+        ns += soff[s2 + 1] - soff[s2];
+      }
+    // sorted position of column c of the concatenation (distinct targets, c < ns)
+    auto col_src = [&](int c) -> int {
+      if (SELF) return sb + c;
+      for (int k = 0;; ++k) {
+        const int s2 = near[(int64_t)t * FMM_NEAR_MAX + k];
+        const int b2 = soff[s2], n2 = soff[s2 + 1] - b2;
+        if (c < n2) return b2 + c;
+        c -= n2;
+      }
+    };
     const bool write_rows = t >= lo && t < hi;
     const bool write_react = sym && s >= lo && s < hi;
-    // ns <= P2P_S: the sources (padded to a multiple of 32) stay in shared memory for the task
-    // and the reactions accumulate there; larger leaves are restaged per row step and chunk
-    const bool whole = ns <= P2P_S;
-    if (whole) {
+    // ns <= P2P_S (P2P_SD): the sources (padded to a multiple of 32) stay in shared memory for
+    // the task and the reactions accumulate there; larger leaves are restaged per row step and chunk
+    const bool whole = ns <= (SELF ? P2P_S : P2P_SD);
+    if (whole && !SELF) {
+      int off = 0;
+      for (int k = 0; k < nn; ++k) {
+        const int s2 = near[(int64_t)t * FMM_NEAR_MAX + k];
+        const int b2 = soff[s2], n2 = soff[s2 + 1] - b2;
+        for (int i = lane; i < n2; i += 32) {
+          s_xy[off + i] = sxy[b2 + i];
+          s_u[off + i] = su[b2 + i];
+        }
+        off += n2;
+      }
+      for (int i = ns + lane; i < ((ns + 31) & ~31); i += 32) {
+        s_xy[i] = make_double2(-P2P_PAD, P2P_PAD);
+        s_u[i] = 0.0;
+      }
+      __syncwarp();
+    } else if (whole) {
       for (int i = lane; i < ((ns + 31) & ~31); i += 32) {
         if (i < ns) {
           s_xy[i] = sxy[sb + i];
@@ -252,8 +299,9 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
       for (int c0 = sd ? (rc & ~31) : 0; c0 < ns; c0 += 32) {
         if (!whole) {
           if (c0 + lane < ns) {
-            s_xy[lane] = sxy[sb + c0 + lane];
-            s_u[lane] = su[sb + c0 + lane];
+            const int i = col_src(c0 + lane);
+            s_xy[lane] = sxy[i];
+            s_u[lane] = su[i];
           } else {
             s_xy[lane] = make_double2(-P2P_PAD, P2P_PAD);
             s_u[lane] = 0.0;
@@ -599,8 +647,9 @@ int fmm_stage_p2p_pairs(fmm_tree_s* t) {
   auto launch = [&](auto kern) -> int {
     FMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_SMEM));
     kern<<<148 * P2P_MINB, 32 * P2P_WARPS, P2P_SMEM, s>>>(t->tasks, t->ntask, t->next_task, t->toff, t->soff, t->txy,
-                                                           t->sxy, t->su, t->near, t->tperm, t->p2p_tab, t->part,
-                                                           G.nslot, t->leaf_lo, t->leaf_hi, t->status);
+                                                           t->sxy, t->su, t->near, t->nnear, t->tperm, t->p2p_tab,
+                                                           t->part, fmm_part_slots(G), t->leaf_lo, t->leaf_hi,
+                                                           t->status);
     return FMM_OK;
   };
   int e = G.self_mode ? launch(k_p2p_pairs<true>) : launch(k_p2p_pairs<false>);
@@ -615,13 +664,14 @@ int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi) {
   cudaStream_t s = t->stream;
   const int64_t nl = t->leaf_hi - t->leaf_lo;
   if (nl > 0)
-    switch (G.nslot) {
+    switch (fmm_part_slots(G)) {
 #define FMM_FINISH(NS)                                                                                        \
   case NS:                                                                                                    \
     k_p2p_finish<NS><<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(                                       \
         t->leaf_lo, t->leaf_hi, t->toff, t->nnear, t->txy, t->centre + G.lvl_off[G.L],                        \
-        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, G.nslot, phi);                             \
+        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, NS, phi);                                  \
     break;
+      FMM_FINISH(1)
       FMM_FINISH(7)
       FMM_FINISH(9)
       FMM_FINISH(13)
