@@ -33,15 +33,19 @@ std::vector<double> host_binom() {
 // tables of p2p_math.cuh, computed once in extended precision (x87 long double)
 void fmm_host_p2p_tables(double* tab) {
   memset(tab, 0, sizeof(double) * P2P_TAB_DOUBLES);  // unused atan slots k = 65..127 read as 0
-  for (int i = 0; i < P2P_LOG_N; ++i) {
-    // interval centre: the value of the centre bit pattern (exactly 1.0 for the interval of 1.0)
-    uint64_t mid = P2P_LOG_OFF + ((uint64_t)i << P2P_LOG_SHIFT) + ((uint64_t)1 << (P2P_LOG_SHIFT - 1));
-    double c;
-    memcpy(&c, &mid, 8);
-    double invc = 1.0 / c;
-    tab[P2P_TAB_LOG + 2 * i] = invc;
-    tab[P2P_TAB_LOG + 2 * i + 1] = (double)(-logl((long double)invc));
-  }
+  // log tables: N intervals centred on the bit patterns of p2p_math.cuh (1.0 is a centre)
+  auto log_table = [&](int off, int n, unsigned long long OFF, int shift) {
+    for (int i = 0; i < n; ++i) {
+      uint64_t mid = OFF + ((uint64_t)i << shift) + ((uint64_t)1 << (shift - 1));
+      double c;
+      memcpy(&c, &mid, 8);
+      double invc = 1.0 / c;
+      tab[off + 2 * i] = invc;
+      tab[off + 2 * i + 1] = (double)(-logl((long double)invc));
+    }
+  };
+  log_table(P2P_TAB_LOG, P2P_LOG_N, P2PLogTab<P2P_LOG_N>::OFF, P2PLogTab<P2P_LOG_N>::SHIFT);
+  log_table(P2P_TAB_LOGC, P2P_LOGC_N, P2PLogTab<P2P_LOGC_N>::OFF, P2PLogTab<P2P_LOGC_N>::SHIFT);
   const long double PI = acosl(-1.0L);
   for (int oct = 0; oct < 8; ++oct) {
     int swap = oct & 1, dxneg = (oct >> 1) & 1, dyneg = (oct >> 2) & 1;

@@ -5,9 +5,10 @@
 // pair loop ~4x slower.  Valid for |z| >= 1e-30 (the caller sends
 // smaller |z|, including the excluded / coincident z = 0, to an exact slow path).
 //
-//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a 512-entry table of
-//            (1/c_i, log c_i) selected by the top mantissa bits; |r| <= 2^-10;
-//            log1p(r) by its Taylor series to r^5 (truncation < 2^-62.5, < 2^-52.5 |r|).
+//   log(r2): r2 = 2^k z, z in [0.6875, 1.375); z = c_i (1 + r) with a table of (1/c_i, log c_i)
+//            selected by the top mantissa bits: 1024 entries, |r| <= 2^-11 and log1p(r) to r^4
+//            (truncation < 2^-57.3 absolute) in the pair kernel; 512 entries, |r| <= 2^-10 and
+//            log1p(r) to r^5 (truncation < 2^-62.5) in the M2L's b_0 (a smaller shared-memory copy).
 //   atan2  : octant reduction to t = num/den in [0, 1]; t_k = k/64 with k = round(64 t)
 //            from a MUFU.RCP64H estimate; atan t = atan t_k + atan q,
 //            q = (num - t_k den) / (den + t_k num), |q| <= 1/128 + 2^-20;
@@ -20,7 +21,8 @@
 #pragma once
 #include <stdint.h>
 
-#define P2P_LOG_N 512
+#define P2P_LOG_N 1024  // log table of the pair kernel, direct sum and debug hook
+#define P2P_LOGC_N 512  // log table of the M2L (compact tables)
 #define P2P_TW 8  // targets per P2P warp task
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
 #define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
@@ -30,7 +32,8 @@
 #define P2P_TAB_LOG 0
 #define P2P_TAB_ATAN (2 * P2P_LOG_N)
 #define P2P_TAB_ATANC (2 * P2P_LOG_N + 2 * P2P_ATAN_N)  // compact copy: entry oct * 65 + k
-#define P2P_TAB_DOUBLES (P2P_TAB_ATANC + 2 * 8 * (P2P_ATAN_K + 1))
+#define P2P_TAB_LOGC (P2P_TAB_ATANC + 2 * 8 * (P2P_ATAN_K + 1))  // the 512-entry log table
+#define P2P_TAB_DOUBLES (P2P_TAB_LOGC + 2 * P2P_LOGC_N)
 
 // atan table entry of (octant, k), octant bit 0 = swap, bit 1 = dx < 0, bit 2 = dy < 0:
 // k + 128 [dx < 0] + 256 [dy < 0] + 512 [swap], so that the pair kernel forms the index from
@@ -40,11 +43,21 @@ __host__ __device__ inline int p2p_atan_index(int oct, int k) {
 }
 // |z|^2 below this (hi word of 1e-60) takes the exact slow path
 #define P2P_SLOW_HI 0x3379b604
-// z intervals: bit patterns [OFF + i 2^43, OFF + (i+1) 2^43), OFF = 0x3fe6000000000000 - 2^42,
-// so that the bit pattern of 1.0 is the centre of interval 320
-#define P2P_LOG_OFF_HI 0x3fe5fc00
-#define P2P_LOG_OFF 0x3fe5fc0000000000ull
-#define P2P_LOG_SHIFT 43
+// z intervals of an N-entry table: bit patterns [OFF + i 2^S, OFF + (i+1) 2^S), S = 52 - log2 N,
+// OFF = 0x3fe6000000000000 - 2^(S-1), so that the bit pattern of 1.0 is the centre of interval
+// 0.625 N (one binade of bit patterns covers z in [0.6875, 1.375))
+template <int N>
+struct P2PLogTab;
+template <>
+struct P2PLogTab<1024> {
+  static constexpr int SHIFT = 42, OFF_HI = 0x3fe5fe00;
+  static constexpr unsigned long long OFF = 0x3fe5fe0000000000ull;
+};
+template <>
+struct P2PLogTab<512> {
+  static constexpr int SHIFT = 43, OFF_HI = 0x3fe5fc00;
+  static constexpr unsigned long long OFF = 0x3fe5fc0000000000ull;
+};
 
 __constant__ double P2P_C[13] = {
     1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,  // log1p Taylor r^7 .. r^2
@@ -62,11 +75,12 @@ __device__ __forceinline__ void p2p_load_tables(const double* __restrict__ tabs,
   __syncthreads();
 }
 
-// compact copy for p2p_atan2<false>: s_atan[8 * (P2P_ATAN_K + 1)], entry oct * 65 + k
+// compact copies for the M2L: s_log[P2P_LOGC_N] (p2p_log<P2P_LOGC_N>) and, for p2p_atan2<false>,
+// s_atan[8 * (P2P_ATAN_K + 1)], entry oct * 65 + k
 __device__ __forceinline__ void p2p_load_tables_compact(const double* __restrict__ tabs, double2* s_log,
                                                         double2* s_atan) {
   const double2* t2 = (const double2*)tabs;
-  for (int i = threadIdx.x; i < P2P_LOG_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOG / 2 + i];
+  for (int i = threadIdx.x; i < P2P_LOGC_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOGC / 2 + i];
   for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATANC / 2 + i];
   __syncthreads();
 }
@@ -94,30 +108,39 @@ __device__ __forceinline__ uint32_t p2p_smem_addr(const void* p) {
   return r;
 }
 
-// log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (log table in shared memory).
-// The 256 intervals of z are centred so that z = 1 is the centre of its interval
+// log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (N-entry log table in shared memory).
+// The N intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
+template <int N = P2P_LOG_N>
 __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
+  using T = P2PLogTab<N>;
   int hi = __double2hiint(r2), lo = __double2loint(r2);
-  int tmp = hi - P2P_LOG_OFF_HI;
-  int i = (tmp >> (P2P_LOG_SHIFT - 32)) & (P2P_LOG_N - 1);
+  int tmp = hi - T::OFF_HI;
+  int i = (tmp >> (T::SHIFT - 32)) & (N - 1);
   int k = tmp >> 20;  // arithmetic shift
   double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
   const double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
-  // r^5 coefficient rounded to a 20-bit mantissa (SASS immediate): its error
-  // (< 2^-21 relative) times r^5/5 stays below 2^-70 for |r| <= 2^-10
-  double q = fma(r, 0x1.9999900000000p-3 /* ~1/5 */, -0.25);
-  q = fma(q, r, P2P_C[4]);  // 1/3 (full precision)
+  double q;
+  if (N >= 1024) {
+    // |r| <= 2^-11: log1p(r) = r - r^2/2 + r^3/3 - r^4/4, truncation r^5/5 < 2^-57.3
+    q = fma(r, -0.25, P2P_C[4]);  // 1/3 (full precision)
+  } else {
+    // r^5 coefficient rounded to a 20-bit mantissa (SASS immediate): its error
+    // (< 2^-21 relative) times r^5/5 stays below 2^-70 for |r| <= 2^-10
+    q = fma(r, 0x1.9999900000000p-3 /* ~1/5 */, -0.25);
+    q = fma(q, r, P2P_C[4]);  // 1/3 (full precision)
+  }
   q = fma(q, r, -0.5);
   *lz = cl.y + fma(r_2, q, r);  // log c_i + log1p(r)
   *kd = (double)k;
 }
 
+template <int N = P2P_LOG_N>
 __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
   double kd, lz;
-  p2p_log_split(r2, logtab, &kd, &lz);
+  p2p_log_split<N>(r2, logtab, &kd, &lz);
   return fma(kd, P2P_C[10], lz) + kd * P2P_C[11];
 }
 

@@ -345,7 +345,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 template <int P>
 struct DownSmem {
   static constexpr int NB = 8, MT = (P + 8) / 8, KT = P / 4;
-  static constexpr size_t tab = sizeof(double2) * (P2P_LOG_N + 8 * (P2P_ATAN_K + 1));
+  static constexpr size_t tab = sizeof(double2) * (P2P_LOGC_N + 8 * (P2P_ATAN_K + 1));
   static constexpr size_t afr = sizeof(double) * (MT * KT * 32 + 8 * MT);  // + 1/r table
   static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + NB + 32) + sizeof(double) * NB +
                                  sizeof(int) * FMM_CAND_MAX;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   constexpr int NB = S::NB, MT = S::MT, KT = S::KT;
   extern __shared__ double2 dsm[];
   double2* s_log = dsm;
-  double2* s_atan = s_log + P2P_LOG_N;
+  double2* s_atan = s_log + P2P_LOGC_N;
   double* s_afr = (double*)((char*)dsm + S::tab);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char* wb = (char*)dsm + S::tab + S::afr + w * S::warp;
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
         }
         if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
           const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
-          s_lg[s] = make_double2(0.5 * p2p_log(fma(dx, dx, dy * dy), a_log), p2p_atan2<false>(dy, dx, a_atan));
+          s_lg[s] = make_double2(0.5 * p2p_log<P2P_LOGC_N>(fma(dx, dx, dy * dy), a_log), p2p_atan2<false>(dy, dx, a_atan));
           s_q[s] = av[0].x;
         }
       }
