@@ -32,7 +32,7 @@ std::vector<double> host_binom() {
 
 // tables of p2p_math.cuh, computed once in extended precision (x87 long double)
 void fmm_host_p2p_tables(double* tab) {
-  memset(tab, 0, sizeof(double) * P2P_TAB_DOUBLES);  // unused atan slots k = 65..127 read as 0
+  memset(tab, 0, sizeof(double) * P2P_TAB_DOUBLES);
   // log tables: N intervals centred on the bit patterns of p2p_math.cuh (1.0 is a centre)
   auto log_table = [&](int off, int n, unsigned long long OFF, int shift) {
     for (int i = 0; i < n; ++i) {
@@ -47,20 +47,21 @@ void fmm_host_p2p_tables(double* tab) {
   log_table(P2P_TAB_LOG, P2P_LOG_N, P2PLogTab<P2P_LOG_N>::OFF, P2PLogTab<P2P_LOG_N>::SHIFT);
   log_table(P2P_TAB_LOGC, P2P_LOGC_N, P2PLogTab<P2P_LOGC_N>::OFF, P2PLogTab<P2P_LOGC_N>::SHIFT);
   const long double PI = acosl(-1.0L);
-  for (int oct = 0; oct < 8; ++oct) {
+  // (theta, tau) of octant oct and knot k / K: theta = Arg of the knot direction in the octant,
+  // tau = its signed slope tan(theta) (no swap) or -cot(theta) (swap), exactly +-k / K
+  auto atan_entry = [&](int oct, int k, int K, double* out) {
     int swap = oct & 1, dxneg = (oct >> 1) & 1, dyneg = (oct >> 2) & 1;
-    for (int k = 0; k <= P2P_ATAN_K; ++k) {
-      long double a = atanl((long double)k / P2P_ATAN_K);
-      long double t1 = swap ? PI / 2 - a : a;
-      long double t2 = dxneg ? PI - t1 : t1;
-      long double t3 = dyneg ? -t2 : t2;
-      tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k)] = (double)t3;
-      // signed slope: tan(theta) (no swap) or -cot(theta) (swap), exactly +-k / K
-      const double sg = (swap ? -1.0 : 1.0) * ((dxneg ^ dyneg) ? -1.0 : 1.0);
-      tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k) + 1] = sg * (double)k / P2P_ATAN_K;
-      tab[P2P_TAB_ATANC + 2 * (oct * (P2P_ATAN_K + 1) + k)] = tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k)];
-      tab[P2P_TAB_ATANC + 2 * (oct * (P2P_ATAN_K + 1) + k) + 1] = tab[P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k) + 1];
-    }
+    long double a = atanl((long double)k / K);
+    long double t1 = swap ? PI / 2 - a : a;
+    long double t2 = dxneg ? PI - t1 : t1;
+    long double t3 = dyneg ? -t2 : t2;
+    out[0] = (double)t3;
+    const double sg = (swap ? -1.0 : 1.0) * ((dxneg ^ dyneg) ? -1.0 : 1.0);
+    out[1] = sg * (double)k / K;
+  };
+  for (int oct = 0; oct < 8; ++oct) {
+    for (int k = 0; k < P2P_ATAN_SUB; ++k) atan_entry(oct, k, P2P_ATAN_KS, tab + P2P_TAB_ATAN + 2 * p2p_atan_index(oct, k));
+    for (int k = 0; k <= P2P_ATAN_K; ++k) atan_entry(oct, k, P2P_ATAN_K, tab + P2P_TAB_ATANC + 2 * (oct * (P2P_ATAN_K + 1) + k));
   }
 }
 

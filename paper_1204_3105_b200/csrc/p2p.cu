@@ -550,14 +550,16 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
 // (fast path, exact slow path for |z| < 1e-30).  Coincident pairs (other than i == j in self
 // mode) set *bad to the smallest target index involved.
 constexpr int DIR_T = 128;
+constexpr size_t DIR_SMEM = sizeof(double2) * (P2P_LOG_N + P2P_ATAN_N + DIR_T) + sizeof(double) * DIR_T;
 __global__ void __launch_bounds__(DIR_T) k_direct(const double2* __restrict__ sxy, const double* __restrict__ su,
                                                   int64_t n, const double2* __restrict__ txy, int64_t m,
                                                   int self_mode, const double* __restrict__ tabs,
                                                   double2* __restrict__ phi, unsigned long long* bad) {
-  __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[P2P_ATAN_N];
-  __shared__ double2 s_x[DIR_T];
-  __shared__ double s_u[DIR_T];
+  extern __shared__ double2 dir_smem[];  // DIR_SMEM bytes: tables, then the staged sources
+  double2* s_log = dir_smem;
+  double2* s_atan = s_log + P2P_LOG_N;
+  double2* s_x = s_atan + P2P_ATAN_N;
+  double* s_u = (double*)(s_x + DIR_T);
   p2p_load_tables(tabs, s_log, s_atan);
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int64_t j = blockIdx.x * (int64_t)DIR_T + threadIdx.x;
@@ -604,8 +606,9 @@ __global__ void __launch_bounds__(DIR_T) k_direct(const double2* __restrict__ sx
 // debug hook: the P2P math on explicit (dx, dy) pairs -> (log |z|^2, Arg z)
 __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const double* __restrict__ tabs,
                                  double2* __restrict__ out) {
-  __shared__ double2 s_log[P2P_LOG_N];
-  __shared__ double2 s_atan[P2P_ATAN_N];
+  extern __shared__ double2 dbg_smem[];  // the P2P tables (P2P_TAB_BYTES)
+  double2* s_log = dbg_smem;
+  double2* s_atan = s_log + P2P_LOG_N;
   p2p_load_tables(tabs, s_log, s_atan);
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -685,15 +688,17 @@ int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi) {
 
 int fmm_direct_launch(const double* sxy, const double* su, int64_t n, const double* txy, int64_t m, int self_mode,
                       const double* tabs, double* phi, unsigned long long* bad, cudaStream_t s) {
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DIR_SMEM));
   if (m > 0)
-    k_direct<<<(unsigned)((m + DIR_T - 1) / DIR_T), DIR_T, 0, s>>>((const double2*)sxy, su, n, (const double2*)txy, m,
+    k_direct<<<(unsigned)((m + DIR_T - 1) / DIR_T), DIR_T, DIR_SMEM, s>>>((const double2*)sxy, su, n, (const double2*)txy, m,
                                                                   self_mode, tabs, (double2*)phi, bad);
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }
 
 int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s) {
-  k_debug_p2p_math<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const double2*)dxdy, n, tabs, (double2*)out);
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_debug_p2p_math, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2P_TAB_BYTES));
+  k_debug_p2p_math<<<(unsigned)((n + 255) / 256), 256, P2P_TAB_BYTES, s>>>((const double2*)dxdy, n, tabs, (double2*)out);
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
 }

@@ -25,9 +25,10 @@
 #define P2P_LOGC_N 512  // log table of the M2L (compact tables)
 #define P2P_TW 8  // targets per P2P warp task
 #define P2P_G 4   // source phases per task (P2P_TW * P2P_G = 32 lanes)
-#define P2P_ATAN_K 64  // t_k = k / 64, k = 0..64
-// table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (theta[oct][k], tau[oct][k]), 8 x (K+1)
-#define P2P_ATAN_SUB 128  // entries per octant sub-table (k = 0..64 used; 65..127 absorb masked garbage)
+#define P2P_ATAN_K 64    // M2L (compact table): t_k = k / 64, k = 0..64
+#define P2P_ATAN_KS 256  // pair kernel (sparse table): t_k = k / 256, k = 0..255 (256 clamps to 255)
+// table layout (doubles): [0, 2N) log (1/c, log c) pairs; then (theta[oct][k], tau[oct][k])
+#define P2P_ATAN_SUB 256  // entries per octant sub-table of the sparse layout
 #define P2P_ATAN_N (8 * P2P_ATAN_SUB)
 #define P2P_TAB_LOG 0
 #define P2P_TAB_ATAN (2 * P2P_LOG_N)
@@ -36,7 +37,7 @@
 #define P2P_TAB_DOUBLES (P2P_TAB_LOGC + 2 * P2P_LOGC_N)
 
 // atan table entry of (octant, k), octant bit 0 = swap, bit 1 = dx < 0, bit 2 = dy < 0:
-// k + 128 [dx < 0] + 256 [dy < 0] + 512 [swap], so that the pair kernel forms the index from
+// k + 256 [dx < 0] + 512 [dy < 0] + 1024 [swap], so that the pair kernel forms the index from
 // the sign bytes of dx, dy with one PRMT (p2p_atan2<true>)
 __host__ __device__ inline int p2p_atan_index(int oct, int k) {
   return k + P2P_ATAN_SUB * ((oct >> 1) & 1) + 2 * P2P_ATAN_SUB * ((oct >> 2) & 1) + 4 * P2P_ATAN_SUB * (oct & 1);
@@ -147,26 +148,30 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // Arg(dx + i dy) in (-pi, pi] for |z| >= 1e-30.  dy must not be -0: callers pass a
 // canonical +0 imaginary zero (D13; the sorted coordinates are canonicalised at the gather,
 // so y - x never yields -0 there).
-// SPARSE: atab holds P2P_ATAN_N entries in the p2p_atan_index layout (pair kernel, direct
-// sum, debug hook); else the compact 8 x 65 copy (M2L), where k must be <= 64 (|z| normal)
+// SPARSE: atab holds P2P_ATAN_N entries in the p2p_atan_index layout with knots k / 256 (pair
+// kernel, direct sum, debug hook): |q| <= 1/512, atan q to q^5 (truncation < 2^-56.8 |q|);
+// else the compact 8 x 65 copy with knots k / 64 (M2L), where k must be <= 64 (|z| normal):
+// |q| <= 1/128, atan q to q^7
 template <bool SPARSE>
 __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
   // Rotation by the reference direction theta of (octant, k): with (P, Q) = (dy, dx), or
   // (-dx, dy) when |dy| > |dx|, and the table's signed slope tau (+-k/64; its sign folds the
   // octant's orientation), Arg z = theta + atan(q), q = (P - tau Q) / (Q + tau P) -- no sign
-  // fix-up.  k = round(64 |P| / |Q|) from the MUFU reciprocal (~2^-22) and the 1.5 2^52 shift.
+  // fix-up.  k = round(K |P| / |Q|) from the MUFU reciprocal (~2^-22) and the 1.5 2^52 shift.
   const bool swap = fabs(dy) > fabs(dx);
   const double P = swap ? -dx : dy, Q = swap ? dy : dx;
   double r0;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(Q));
-  const int k = __double2loint(fma(fabs(P * r0), (double)P2P_ATAN_K, 6755399441055744.0));  // 0..64 (masked below)
+  const int k = __double2loint(fma(fabs(P * r0), SPARSE ? (double)P2P_ATAN_KS : (double)P2P_ATAN_K,
+                                   6755399441055744.0));  // 0..K (clamped / masked below)
   const int hx = __double2hiint(dx), hy = __double2hiint(dy);
   uint32_t idx;
   if (SPARSE) {
-    // byte 0 = sign of dx replicated (bit 7 -> +128), byte 1 = sign of dy (bit 8 -> +256)
+    // byte 0 = sign of dx replicated (bit 7), byte 1 = sign of dy (bit 8), shifted to +256 / +512;
+    // k = 256 (t = 1 within rounding) and the garbage k of |z| < 1e-30 clamp to 255 (|q| <= 1/512)
     uint32_t sg;
     asm("prmt.b32 %0, %1, %2, 0xFB;" : "=r"(sg) : "r"(hx), "r"(hy));
-    idx = ((uint32_t)k & 0x7fu) | (sg & 0x180u) | (swap ? 4u * P2P_ATAN_SUB : 0u);
+    idx = ((sg & 0x180u) << 1) + min((uint32_t)k, (uint32_t)(P2P_ATAN_SUB - 1)) + (swap ? 4u * P2P_ATAN_SUB : 0u);
   } else {
     // octant: bit0 swap, bit1 dx < 0, bit2 dy < 0
     const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
@@ -183,8 +188,13 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   e = fma(e, e, e);
   const double q = fma(q0, e, q0);
   const double q2 = q * q;
-  // q^7 coefficient rounded to a 20-bit mantissa (immediate), error < 2^-62 |q|
-  double Pq = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
-  Pq = fma(Pq, q2, P2P_C[9]);  // -1/3
+  double Pq;
+  if (SPARSE) {
+    Pq = fma(q2, P2P_C[8] /* 1/5 */, P2P_C[9] /* -1/3 */);
+  } else {
+    // q^7 coefficient rounded to a 20-bit mantissa (immediate), error < 2^-62 |q|
+    Pq = fma(q2, -0x1.2492400000000p-3 /* ~-1/7 */, P2P_C[8] /* 1/5 */);
+    Pq = fma(Pq, q2, P2P_C[9]);  // -1/3
+  }
   return Tt.x + fma(q * q2, Pq, q);
 }
