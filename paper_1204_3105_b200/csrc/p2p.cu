@@ -427,13 +427,12 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
         if (hw) {  // lane c owns column c of the chunk: add its 4 row-lane partials (fixed order)
           __syncwarp();
           double Rr = 0.0, Ri = 0.0;
-          if ((hw >> (lane >> 4)) & 1) {
+          if ((hw >> (lane >> 4)) & 1) {  // pairwise: (r0 + r1) + (r2 + r3)
+            double2 v[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const double2 v = s_rs[r * P2P_RS + (lane ^ (2 * r))];
-              Rr += v.x;
-              Ri += v.y;
-            }
+            for (int r = 0; r < 4; ++r) v[r] = s_rs[r * P2P_RS + (lane ^ (2 * r))];
+            Rr = (v[0].x + v[1].x) + (v[2].x + v[3].x);
+            Ri = (v[0].y + v[1].y) + (v[2].y + v[3].y);
           }
           if (whole) {
             const double2 o = s_re[cb + lane];
@@ -462,9 +461,10 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
       if (lane < 16) {
         const double* sd_ = (const double*)s_rs;
         const int rr = lane >> 1, comp = lane & 1;
-        double v = 0.0;
+        double a[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v += sd_[(k * 8 + rr) * 2 + comp];
+        for (int k = 0; k < 8; ++k) a[k] = sd_[(k * 8 + rr) * 2 + comp];
+        const double v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));  // pairwise
         const int row = rc + (rr & 3) + 4 * (rr >> 2);
         if (row < tk.w) {
           if (sd && whole) {  // rows and reactions of a diagonal block share the slots: add into s_re
