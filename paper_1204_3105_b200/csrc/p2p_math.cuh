@@ -158,8 +158,16 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
   // (-dx, dy) when |dy| > |dx|, and the table's signed slope tau (+-k/64; its sign folds the
   // octant's orientation), Arg z = theta + atan(q), q = (P - tau Q) / (Q + tau P) -- no sign
   // fix-up.  k = round(K |P| / |Q|) from the MUFU reciprocal (~2^-22) and the 1.5 2^52 shift.
-  const bool swap = fabs(dy) > fabs(dx);
-  const double P = swap ? -dx : dy, Q = swap ? dy : dx;
+  // swap = |dy| > |dx|, decided in FP32 on the high words (sign, 11-bit exponent, 20 mantissa
+  // bits read as a float: monotonic in the magnitude for |x| < 2^1017) instead of a DSETP on the
+  // FP64 pipe; a tie in the high words leaves swap false with |P| / |Q| < 1 + 2^-20, which the
+  // sparse table's k <= 255 clamp covers (|q| <= 1/512 + 2^-20).  The compact (M2L) path keeps
+  // the exact test (its k is masked, not clamped).
+  const int hx0 = __double2hiint(dx), hy0 = __double2hiint(dy);
+  const bool swap = SPARSE ? fabsf(__int_as_float(hy0)) > fabsf(__int_as_float(hx0)) : fabs(dy) > fabs(dx);
+  // -dx by a sign-bit flip of the high word (an ALU op, not a DADD on the FP64 pipe)
+  const double ndx = __hiloint2double(hx0 ^ (int)0x80000000, __double2loint(dx));
+  const double P = swap ? ndx : dy, Q = swap ? dy : dx;
   double r0;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(Q));
   const int k = __double2loint(fma(fabs(P * r0), SPARSE ? (double)P2P_ATAN_KS : (double)P2P_ATAN_K,
