@@ -53,19 +53,22 @@ WORKLOADS = {
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # SURVEY §8(d) algorithmic work per unit:
 #  * P2P: F_pair FP64 flops per near-field interaction (ordered target-source pair), measured by
-#    ncu on the one-pair-per-thread microbenchmark tools/fpair_micro.py: 44 flops of math
-#    (|z|^2, log|z|^2, Arg z) + 2 DADD (y - x) + 2 DFMA (strength products) = 50
-#    (profiles/r01/fp64_counts.json, re-measured after every change of the pair math).  The symmetric self-mode kernel evaluates each unordered
+#    ncu on the one-pair-per-thread microbenchmark tools/fpair_micro.py: 39 flops of math
+#    (|z|^2, log|z|^2, Arg z) + 2 DADD (y - x) + 2 DFMA (strength products) = 45
+#    (profiles/r02/fp64_counts.json, re-measured after every change of the pair math: 50 in
+#    round 1; the 1024-entry log table and the k/256 atan knots each removed a DFMA).  The symmetric self-mode kernel evaluates each unordered
 #    pair once, so it executes fewer flops than this per interaction (reported beside it).
 #  * M2L: the dense-operator count 8 (p+1)^2 flops per M2L op.
-F_PAIR = 50.0
+F_PAIR = 45.0
 # FP64 flops k_p2p_pairs executes per interaction (ncu, sm__sass_thread_inst_executed_op_
-# {dfma,dadd,dmul}_pred_on; profiles/r01/fp64_counts.json), for the executed-rate line
-F_EXEC = {"C4q": 30.03, "C4s": 27.95, "C4t": 29.79, "C3": 54.55, "C5": 26.59}
-# dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu --set full,
-# profiles/r01/ncu_p2p_<cfg>_v16.txt, unchanged within 1 % in _v25); C4 = mean over its three launches.  The writes are the
-# per-(target, near slot) partial sums (m x nslot x 16 B) that k_p2p_finish adds.
-P2P_DRAM_BYTES_PER_LAUNCH = {"C4q": 2.847e9, "C4s": 2.411e9, "C4t": 3.995e9, "C4": 3.084e9}
+# {dfma,dadd,dmul}_pred_on; profiles/r02/fp64_counts.json), for the executed-rate line
+F_EXEC = {"C4q": 27.01, "C4s": 25.14, "C4t": 26.79, "C3": 44.48, "C5": 23.91}
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu, profiles/r02/ncu/
+# dram_<cfg>.csv); C4 = mean over its three launches.  The self-mode writes are the per-(target,
+# near slot) partial sums (m x nslot x 16 B) that k_p2p_finish adds; distinct targets (C3) write
+# one slot per target.
+P2P_DRAM_BYTES_PER_LAUNCH = {"C4q": 2.841e9, "C4s": 2.378e9, "C4t": 3.989e9, "C4": 3.069e9, "C3": 0.228e9,
+                             "C5": 3.157e9}
 
 
 def log(*a):
