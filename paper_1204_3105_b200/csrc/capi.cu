@@ -201,7 +201,7 @@ void carve(fmm_tree_s* t, Arena& a) {
   t->nnear = a.take<int32_t>(K);
   // every (leaf, near leaf) block gives at most ceil(rows / 8) tasks
   t->ntask_cap = (int64_t)G.nslot * (m / 8 + G.K) + 1;
-  t->tasks = a.take<int4>(t->ntask_cap);
+  t->tasks = a.take<int4>(2 * t->ntask_cap);  // two int4 per task (p2p.cu leaf_tasks)
   t->part = a.take<double2>((m + 1) * (int64_t)fmm_part_slots(G));
   t->ntask = a.take<int32_t>(1);
   t->next_task = a.take<int32_t>(1);

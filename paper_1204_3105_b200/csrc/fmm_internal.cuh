@@ -76,7 +76,8 @@ struct fmm_tree_s {
   int32_t* near;   // [K][FMM_NEAR_MAX]
   int32_t* nnear;  // [K]
   // P2P work list
-  int4* tasks;         // [ntask_cap] (leaf t, q | q_rev << 8 | flags, row0, row1) of p2p.cu
+  int4* tasks;         // [2 ntask_cap] per task (leaf t, q | q_rev << 8 | flags, row0, row1), (first target of t, first
+                       // source / count of the columns, column leaf) of p2p.cu
   double2* part;       // [m][nslot] per (target, near-leaf) partial sums (Re, Im) of the near field
   int32_t* ntask;      // [1] device counter
   int32_t* next_task;  // [1] dynamic scheduling counter of the P2P kernel

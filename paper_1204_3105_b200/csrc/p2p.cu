@@ -42,12 +42,21 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
   const bool t_in = t >= lo && t < hi;
   const int nn = nnear[t];
   int c = 0;
+  // a task is two int4: (row leaf, slot | reverse slot << 8 | flags, row range) and the values the
+  // pair kernel would otherwise load one after another (first sorted target of the row leaf,
+  // first source and source count of the column leaf -- all near leaves for distinct targets --,
+  // column leaf)
+  auto put = [&](int4 a, int ncols) {
+    if (out) {
+      const int s = near[(int64_t)a.x * FMM_NEAR_MAX + (a.y & 0xff)];
+      out[2 * c] = a;
+      out[2 * c + 1] = make_int4(toff[a.x], soff[s], ncols, s);
+    }
+    ++c;
+  };
   auto emit_rows = [&](int leaf, int qq, int rows, int ns, int flags) {
     const int rs = split_rows(ns);
-    for (int r0 = 0; r0 < rows; r0 += rs) {
-      if (out) out[c] = make_int4(leaf, qq | flags, r0, min(rows, r0 + rs));
-      ++c;
-    }
+    for (int r0 = 0; r0 < rows; r0 += rs) put(make_int4(leaf, qq | flags, r0, min(rows, r0 + rs)), ns);
   };
   if (!self_mode) {
     // distinct targets: one task (row ranges of <= 65,536 pairs) over ALL near leaves of t, their
@@ -68,8 +77,7 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
     if (s == t) {  // diagonal block: symmetric (each unordered pair once) when it fits a warp
       if (t_in) {
         if (ns <= P2P_S) {
-          if (out) out[c] = make_int4(t, q | (q << 8) | TF_SYM | TF_DIAG, 0, nt);
-          ++c;
+          put(make_int4(t, q | (q << 8) | TF_SYM | TF_DIAG, 0, nt), ns);
         } else {
           // heavy diagonal: symmetric row ranges; rows and reactions meet in slot q and are
           // added atomically (zeroed by k_heavy_zero)
@@ -85,8 +93,7 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
       if (near[(int64_t)s * FMM_NEAR_MAX + k] == t) qr = k;
     if ((int64_t)nt * ns <= P2P_LIGHT) {
       if (t_in || s_in) {
-        if (out) out[c] = make_int4(t, q | (qr << 8) | TF_SYM, 0, nt);
-        ++c;
+        put(make_int4(t, q | (qr << 8) | TF_SYM, 0, nt), ns);
       }
     } else if (t_in || s_in) {
       // heavy block: symmetric too, split by rows of the larger leaf; the smaller one is the
@@ -106,9 +113,9 @@ __global__ void k_heavy_zero(const int4* __restrict__ tasks, const int32_t* __re
                              double2* __restrict__ part, int nslot) {
   const int ntask = *ntask_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntask; i += (int64_t)gridDim.x * blockDim.x) {
-    const int4 tk = tasks[i];
+    const int4 tk = tasks[2 * i];
     if (!(tk.y & TF_HEAVY) || tk.z != 0) continue;
-    const int s = near[(int64_t)tk.x * FMM_NEAR_MAX + (tk.y & 0xff)], qr = (tk.y >> 8) & 0xff;
+    const int s = tasks[2 * i + 1].w, qr = (tk.y >> 8) & 0xff;
     for (int j = soff[s]; j < soff[s + 1]; ++j) part[(int64_t)j * nslot + qr] = make_double2(0.0, 0.0);
   }
 }
@@ -131,7 +138,7 @@ __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const i
     *ntask = start[K];
     return;
   }
-  leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, tasks + start[t]);
+  leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, tasks + 2 * (int64_t)start[t]);
 }
 
 // ------------------------------------------------------------------ the pair kernel
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     if (lane == 0) task = atomicAdd(next_task, 1);
     task = __shfl_sync(0xffffffffu, task, 0);
     if (task >= ntask) break;
-    const int4 tk = tasks[task];
+    const int4 tk = tasks[2 * task];
     const int t = tk.x, q = tk.y & 0xff, qr = (tk.y >> 8) & 0xff;
     const bool sym = SELF && (tk.y & TF_SYM), diag = SELF && (tk.y & TF_DIAG), heavy = SELF && (tk.y & TF_HEAVY);
     // symmetric diagonal block: a row step of rows [rc, rc + 8) and a 16-column half at a
@@ -231,16 +238,24 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     // excluded z = 0) and symmetrically when it lies above them; each ordered pair i != j
     // is then counted once (tests/test_p2p_schedule.py enumerates the rule)
     const bool sd = sym && diag;
-    const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
-    const int tb = toff[t];
+    // distinct targets: first target of t, count of the concatenated columns from the task's
+    // second half (one memory round trip); self mode: loaded here, which keeps the symmetric
+    // kernel's register allocation (holding the second half through the pair loop cost it 1.5 %)
+    int tb, sb, ns, s;
+    if (SELF) {
+      s = near[(int64_t)t * FMM_NEAR_MAX + q];
+      tb = toff[t];
+      sb = soff[s];
+      ns = soff[s + 1] - sb;
+    } else {
+      const int4 tx = tasks[2 * task + 1];
+      tb = tx.x;
+      sb = tx.y;
+      ns = tx.z;
+      s = tx.w;
+    }
     // distinct targets: the columns are the sources of all near leaves of t, concatenated
     const int nn = SELF ? 1 : nnear[t];
-    int sb = soff[s], ns = soff[s + 1] - sb;
-    if (!SELF)
-      for (int k = 1; k < nn; ++k) {
-        const int s2 = near[(int64_t)t * FMM_NEAR_MAX + k];
-        ns += soff[s2 + 1] - soff[s2];
-      }
     // sorted position of column c of the concatenation (distinct targets, c < ns)
     auto col_src = [&](int c) -> int {
       if (SELF) return sb + c;
