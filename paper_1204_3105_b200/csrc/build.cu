@@ -37,20 +37,25 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
                                               const double* __restrict__ u = nullptr,
                                               double2* __restrict__ rec = nullptr,
                                               int32_t* __restrict__ hist = nullptr) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double2 p = xy[i];
-  if (rec) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
-    rec[2 * i] = p;
-    rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  uint32_t k = 0xffffffffu;  // lanes past n: a key no point has (they form their own match group)
+  if (valid) {
+    const double2 p = xy[i];
+    if (rec) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
+      rec[2 * i] = p;
+      rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+    }
+    if (!geo_key(g, p.x, p.y, &k)) {
+      k = (uint32_t)g.K;
+      atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
+    }
+    key[i] = k;
   }
-  uint32_t k;
-  if (!geo_key(g, p.x, p.y, &k)) {
-    k = (uint32_t)g.K;
-    atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
+  if (hist) {  // leaf histogram of every point, one atomic per distinct key of the warp
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[k], __popc(peers));
   }
-  key[i] = k;
-  if (hist) atomicAdd(&hist[k], 1);  // multi-rank: global leaf histogram of every point
 }
 
 // leaf CSR from the sorted keys: off[k] = #points with key < k, k = 0..K+1; position i
@@ -386,6 +391,119 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
       rec_out[2 * g + 1] = b;
     }
   }
+}
+
+// ------------------------------------------------------------------ bucket sort (one rank)
+// Stable order by (key, input index) in three streaming passes instead of two LSD radix passes:
+// the keying kernel counts every leaf (k_keys with hist), the exclusive scan of the counts is the
+// leaf CSR itself, k_bucket_scatter drops each point's 32-byte record (x, y, u, input index)
+// into its leaf's range at an atomically claimed slot (one atomic per distinct key of a warp),
+// and k_leaf_order restores input order inside each leaf (a warp ranks each record by counting
+// the smaller input indices of its leaf) while writing the sorted SoA arrays and the
+// permutation.  The scatter is bound by the L2's atomic throughput per leaf counter and the
+// ranking is quadratic in the leaf size, so the bucket sort serves small leaves only: trees
+// with more than LO_MEAN_MAX points per leaf on average, or with a leaf above LO_WARP_MAX
+// points, take the LSD record sort (measured: DESIGN.md §8c).
+constexpr int LO_WARP_MAX = 256;  // points of a leaf ordered by one warp
+constexpr int LO_MEAN_MAX = 80;   // mean points per leaf above which the LSD sort is taken directly
+
+__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ key,
+                                                        const double2* __restrict__ xy,
+                                                        const double* __restrict__ u, int64_t n,
+                                                        const int32_t* __restrict__ off, int32_t* __restrict__ cur,
+                                                        double2* __restrict__ rec) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool v = i < n;
+  const uint32_t k = v ? key[i] : 0xffffffffu;
+  // one atomic per distinct key of the warp; its lanes take consecutive slots in lane order
+  const unsigned peers = __match_any_sync(0xffffffffu, k);
+  const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+  int base = 0;
+  if (v && lane == leader) base = atomicAdd(&cur[k], __popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!v) return;
+  const int64_t pos = (int64_t)off[k] + base + __popc(peers & ((1u << lane) - 1u));
+  const double2 p = xy[i];
+  rec[2 * pos] = p;
+  rec[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+}
+
+__device__ __forceinline__ int rec_index(const double2* __restrict__ rec, int64_t pos) {
+  return (int)__double_as_longlong(rec[2 * pos + 1].y);
+}
+
+// the record at bucket position pos goes to sorted position o: coordinates with a canonical +0
+// for a -0 (D13, p2p.cu), strength, input index
+__device__ __forceinline__ void lo_write(const double2* __restrict__ rec, int64_t pos, int64_t o,
+                                        double2* __restrict__ sxy, double* __restrict__ su,
+                                        int32_t* __restrict__ perm) {
+  const double2 a = rec[2 * pos], b = rec[2 * pos + 1];
+  sxy[o] = make_double2(__dadd_rn(a.x, 0.0), __dadd_rn(a.y, 0.0));
+  if (su) su[o] = b.x;
+  perm[o] = (int)__double_as_longlong(b.y);
+}
+
+// one warp per bucket (K + 1 buckets: the leaves and the out-of-domain sentinel K): rank of each
+// record = number of records of the bucket with a smaller input index (indices are distinct)
+template <int R>
+__device__ __forceinline__ void lo_rank_warp(const int* __restrict__ sidx, int n, int lane, int64_t b,
+                                             const double2* __restrict__ rec, double2* __restrict__ sxy,
+                                             double* __restrict__ su, int32_t* __restrict__ perm) {
+  int mine[R], rank[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    mine[r] = lane + 32 * r < n ? sidx[lane + 32 * r] : INT_MAX;
+    rank[r] = 0;
+  }
+  for (int j = 0; j < n; ++j) {
+    const int v = sidx[j];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rank[r] += v < mine[r];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (lane + 32 * r < n) lo_write(rec, b + lane + 32 * r, b + rank[r], sxy, su, perm);
+}
+
+__global__ void __launch_bounds__(256) k_leaf_order(int64_t nbuckets, const int32_t* __restrict__ off,
+                                                    const double2* __restrict__ rec, double2* __restrict__ sxy,
+                                                    double* __restrict__ su, int32_t* __restrict__ perm) {
+  __shared__ int sidx[8][LO_WARP_MAX];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k = blockIdx.x * 8ll + w;
+  if (k >= nbuckets) return;
+  const int64_t b = off[k];
+  const int n = off[k + 1] - (int)b;
+  if (n <= 0) return;  // (n <= LO_WARP_MAX: host-checked)
+  int* si = sidx[w];
+  for (int e = lane; e < n; e += 32) si[e] = rec_index(rec, b + e);
+  __syncwarp();
+  if (n <= 32)
+    lo_rank_warp<1>(si, n, lane, b, rec, sxy, su, perm);
+  else if (n <= 64)
+    lo_rank_warp<2>(si, n, lane, b, rec, sxy, su, perm);
+  else if (n <= 128)
+    lo_rank_warp<4>(si, n, lane, b, rec, sxy, su, perm);
+  else
+    lo_rank_warp<8>(si, n, lane, b, rec, sxy, su, perm);
+}
+
+// largest bucket (leaves and the sentinel) of a count array
+__global__ void __launch_bounds__(256) k_max_i32(const int32_t* __restrict__ v, int64_t n, int32_t* __restrict__ mx) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, v[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+// (x, y, u, input index) records in input order (the LSD fallback of the bucket sort)
+__global__ void k_make_rec(const double2* __restrict__ xy, const double* __restrict__ u, int64_t n,
+                           double2* __restrict__ rec) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  rec[2 * i] = xy[i];
+  rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
 }
 
 // ------------------------------------------------------------------ gathers
@@ -929,67 +1047,136 @@ static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64
   return FMM_OK;
 }
 
-int fmm_stage_keys_sort(fmm_tree_s* t) {
+// one rank (DESIGN.md §7 "Build"), per point set: the LSD record sort when the leaves hold more
+// than LO_MEAN_MAX points on average; else keys with leaf counts, the leaf CSR from their scan
+// and, when no leaf holds more than LO_WARP_MAX points (one 8-byte read-back), the bucket sort,
+// otherwise the LSD record sort.  FMM_SORT_LSD=1 forces the LSD sort.
+static int single_rank_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
   DGeo g = dgeo(G);
-  const bool multi = t->cfg.nranks > 1;
-  // one rank: (x, y, u, index) records of sources (and of distinct targets) that the radix sort
-  // carries to their sorted positions
-  double2* rec = nullptr;
-  double2* trec = nullptr;
-  if (multi) {
-    FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (G.K + 2), s));
-    if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (G.K + 2), s));
+  const int64_t K = G.K, nb = K + 2;
+  const int nsets = G.self_mode ? 1 : 2;
+  const int64_t cnt[2] = {t->n, G.self_mode ? 0 : t->m};
+  t->n_loc = t->n;  // one rank keeps every point
+  t->m_loc = t->m;
+  const char* force = getenv("FMM_SORT_LSD");
+  const bool force_lsd = force && force[0] == '1';
+  bool lsd[2];
+  for (int k = 0; k < 2; ++k) lsd[k] = force_lsd || cnt[k] > LO_MEAN_MAX * K;
+  // scratch per point set: counts (K + 2) | scan scratch; then the two maxima
+  const size_t sscan = fmm_scan_scratch_bytes(nb);
+  const size_t hb = ((size_t)nb * 4 + 255) / 256 * 256;
+  const size_t per = hb + (sscan + 255) / 256 * 256;
+  char* buf = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, nsets * per + 256, s));
+  int32_t* mx = (int32_t*)(buf + nsets * per);
+  FMM_CUDA_TRY(cudaMemsetAsync(buf, 0, nsets * per + 256, s));
+  auto hist = [&](int k) { return (int32_t*)(buf + k * per); };
+  auto sscr = [&](int k) { return (void*)(buf + k * per + hb); };
+  const double2* xy[2] = {(const double2*)t->src_xy_in, (const double2*)t->tgt_xy_in};
+  const double* u[2] = {t->src_u_in, nullptr};
+  uint32_t* keys[2] = {t->skey, t->tkey};
+  int32_t* off[2] = {t->soff, t->toff};
+  double2* xy_out[2] = {t->sxy, t->txy};
+  double* u_out[2] = {t->su, nullptr};
+  int32_t* perm[2] = {t->sperm, t->tperm};
+  double2* rec[2] = {nullptr, nullptr};
+  for (int k = 0; k < nsets; ++k)
+    if (cnt[k] > 0) {
+      FMM_CUDA_TRY(cudaMallocAsync((void**)&rec[k], (size_t)cnt[k] * 32, s));
+      // LSD: keys + records in input order (no counts); bucket: keys + counts
+      k_keys<<<blocks_for(cnt[k], 256), 256, 0, s>>>(g, xy[k], cnt[k], k ? t->n : 0, keys[k], t->status,
+                                                      lsd[k] ? u[k] : nullptr, lsd[k] ? rec[k] : nullptr,
+                                                      lsd[k] ? nullptr : hist(k));
+      t->launches++;
+    }
+  FMM_CUDA_TRY(cudaGetLastError());
+  if (t->timing) cudaEventRecord(t->ev[8], s);
+  if (t->timing) cudaEventRecord(t->ev[9], s);
+  int e = FMM_OK;
+  bool need_max = false;
+  for (int k = 0; k < nsets && !e; ++k)
+    if (cnt[k] > 0 && !lsd[k]) {
+      e = fmm_device_scan_i32(hist(k), off[k], nb, sscr(k), sscan, s, &t->launches);
+      k_max_i32<<<64, 256, 0, s>>>(hist(k), K + 1, mx + k);
+      t->launches++;
+      need_max = true;
+    }
+  int32_t hmx[2] = {0, 0};
+  if (!e && need_max) {
+    FMM_CUDA_TRY(cudaMemcpyAsync(hmx, mx, sizeof(hmx), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(cudaStreamSynchronize(s));
   }
+  for (int k = 0; k < nsets && !e; ++k) {
+    if (cnt[k] == 0) {
+      FMM_CUDA_TRY(cudaMemsetAsync(off[k], 0, sizeof(int32_t) * nb, s));
+      continue;
+    }
+    if (!lsd[k] && hmx[k] > LO_WARP_MAX) {  // a large leaf: the LSD sort after all
+      k_make_rec<<<blocks_for(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k]);
+      t->launches++;
+      lsd[k] = true;
+    }
+    if (lsd[k]) {
+      e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k]);
+    } else {
+      double2* brec = rec[k];  // bucket-ordered records (the input-order records were not needed)
+      int32_t* cur = hist(k);  // the counts, zeroed, become the per-leaf slot cursors
+      FMM_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(int32_t) * nb, s));
+      k_bucket_scatter<<<blocks_for(cnt[k], 256), 256, 0, s>>>(keys[k], xy[k], u[k], cnt[k], off[k], cur, brec);
+      k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], brec, xy_out[k], u_out[k], perm[k]);
+      t->launches += 2;
+    }
+    FMM_CUDA_TRY(cudaGetLastError());
+  }
+  for (int k = 0; k < nsets; ++k)
+    if (rec[k]) cudaFreeAsync(rec[k], s);
+  cudaFreeAsync(buf, s);
+  return e;
+}
+
+int fmm_stage_keys_sort(fmm_tree_s* t) {
+  if (t->cfg.nranks <= 1) return single_rank_keys_sort(t);
+  // multi-rank: keys of every point with the global leaf counts, the rank's
+  // selection (compacted keys + input indices of the kept points), their stable radix sort,
+  // then the kept points gathered from the caller's arrays
+  cudaStream_t s = t->stream;
+  const Geo& G = t->g;
+  DGeo g = dgeo(G);
+  FMM_CUDA_TRY(cudaMemsetAsync(t->gsoff, 0, sizeof(int32_t) * (G.K + 2), s));
+  if (!G.self_mode) FMM_CUDA_TRY(cudaMemsetAsync(t->gtoff, 0, sizeof(int32_t) * (G.K + 2), s));
   if (t->n > 0) {
-    if (!multi) FMM_CUDA_TRY(cudaMallocAsync((void**)&rec, (size_t)t->n * 32, s));
     k_keys<<<blocks_for(t->n, 256), 256, 0, s>>>(g, (const double2*)t->src_xy_in, t->n, 0, t->skey, t->status,
-                                                  multi ? nullptr : t->src_u_in, rec, multi ? t->gsoff : nullptr);
+                                                  nullptr, nullptr, t->gsoff);
     t->launches++;
   }
   if (!G.self_mode && t->m > 0) {
-    if (!multi) FMM_CUDA_TRY(cudaMallocAsync((void**)&trec, (size_t)t->m * 32, s));
     k_keys<<<blocks_for(t->m, 256), 256, 0, s>>>(g, (const double2*)t->tgt_xy_in, t->m, t->n, t->tkey, t->status,
-                                                  nullptr, trec, multi ? t->gtoff : nullptr);
+                                                  nullptr, nullptr, t->gtoff);
     t->launches++;
   }
   FMM_CUDA_TRY(cudaGetLastError());
   if (t->timing) cudaEventRecord(t->ev[8], s);
-  // multi-rank: select the kept points first (compacted keys + input indices)
-  uint32_t* ckey = nullptr;
-  int32_t* cidx = nullptr;
-  int e = FMM_OK;
-  t->n_loc = t->n;
-  t->m_loc = t->m;
-  if (multi) {
-    const int64_t tot = t->n + (G.self_mode ? 0 : t->m);
-    char* buf = nullptr;
-    FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, (size_t)tot * 8 + 256, s));
-    ckey = (uint32_t*)buf;
-    cidx = (int32_t*)(buf + (size_t)tot * 4);
-    int64_t* dcount = (int64_t*)(buf + (size_t)tot * 8);
-    e = multi_rank_select(t, ckey, cidx, dcount);
-  }
+  const int64_t tot = t->n + (G.self_mode ? 0 : t->m);
+  char* buf = nullptr;
+  FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, (size_t)tot * 8 + 256, s));
+  uint32_t* ckey = (uint32_t*)buf;
+  int32_t* cidx = (int32_t*)(buf + (size_t)tot * 4);
+  int64_t* dcount = (int64_t*)(buf + (size_t)tot * 8);
+  int e = multi_rank_select(t, ckey, cidx, dcount);
   if (t->timing) cudaEventRecord(t->ev[9], s);
-  // stable sorts; leaf CSR offsets from the sorted keys (soff[K] = #in-domain kept points).
-  // One rank: the records travel with the keys.  Multi-rank: the compacted (key, input index)
-  // pairs are sorted and the kept points gathered from the caller's arrays.
-  if (!e) e = multi ? radix_sort_perm(t, ckey, t->n_loc, t->sperm, t->soff, cidx)
-                    : radix_sort_records(t, t->skey, rec, t->n, t->sxy, t->su, t->sperm, t->soff);
-  if (!e && !G.self_mode)
-    e = multi ? radix_sort_perm(t, ckey + t->n, t->m_loc, t->tperm, t->toff, cidx + t->n)
-              : radix_sort_records(t, t->tkey, trec, t->m, t->txy, nullptr, t->tperm, t->toff);
-  if (ckey) cudaFreeAsync(ckey, s);
-  if (rec) cudaFreeAsync(rec, s);
-  if (trec) cudaFreeAsync(trec, s);
+  // stable sorts of the compacted (key, input index) pairs; leaf CSR offsets from the sorted keys
+  if (!e) e = radix_sort_perm(t, ckey, t->n_loc, t->sperm, t->soff, cidx);
+  if (!e && !G.self_mode) e = radix_sort_perm(t, ckey + t->n, t->m_loc, t->tperm, t->toff, cidx + t->n);
+  cudaFreeAsync(buf, s);
   if (e) return e;
-  if (multi && t->n_loc > 0) {
+  if (t->n_loc > 0) {
     k_gather_src_in<<<blocks_for(t->n_loc, 256), 256, 0, s>>>(t->sperm, t->n_loc, (const double2*)t->src_xy_in,
                                                                t->src_u_in, t->sxy, t->su);
     t->launches++;
   }
-  if (multi && !G.self_mode && t->m_loc > 0) {
+  if (!G.self_mode && t->m_loc > 0) {
     k_gather_xy<<<blocks_for(t->m_loc, 256), 256, 0, s>>>(t->tperm, t->m_loc, (const double2*)t->tgt_xy_in, t->txy);
     t->launches++;
   }

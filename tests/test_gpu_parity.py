@@ -290,3 +290,44 @@ def test_tiny_separation_across_leaves(self_mode):
     assert normwise(phi, ref) <= TOL
     b = g.evaluate().cpu().numpy()
     assert np.array_equal(phi, b)
+
+
+@pytest.mark.parametrize("case", ["bucket", "lsd_mean", "lsd_big_leaf", "lsd_forced"])
+def test_sort_paths_bit_exact(case, monkeypatch):
+    """The one-rank sort (build.cu single_rank_keys_sort) on each of its paths against the
+    oracle's stable order by (key, input index): the bucket sort (small leaves), the LSD
+    record sort taken for a high mean occupancy, the LSD sort taken after the leaf counts show a
+    leaf above 256 points (a tight cluster in an otherwise sparse tree), and FMM_SORT_LSD=1;
+    permutation and leaf CSR bit for bit, potentials within the D15 gate; self mode and distinct
+    targets."""
+    from paper_1204_3105_b200 import X
+
+    base = SMALL_CASES["C4qs"]
+    n, depth = {"bucket": (20000, 4), "lsd_mean": (30000, 2), "lsd_big_leaf": (20000, 4),
+                "lsd_forced": (20000, 4)}[case]
+    if case == "lsd_forced":
+        monkeypatch.setenv("FMM_SORT_LSD", "1")
+    for self_mode in (True, False):
+        w = base.scaled(n, n // 2, name=f"sort-{case}")
+        w.self_mode = self_mode
+        w.m = n if self_mode else n // 2
+        d = dict(data(w))
+        if case == "lsd_big_leaf":  # 400 points within 1e-3 of (0.1, 0.1): one leaf of > 256
+            rng = np.random.default_rng(5)
+            xy = d["src_xy"].copy()
+            xy[:400] = 0.1 + rng.uniform(-1e-3, 1e-3, (400, 2))
+            d["src_xy"] = xy
+        g = gpu_tree(w, d, depth=depth)
+        o = oracle_tree(w, d, depth=depth)
+        sp, tp = o.perm()
+        so, to = o.leaf_offsets()
+        if case == "lsd_big_leaf":
+            assert np.diff(so).max() > 256
+        assert np.array_equal(g.export(X.SRC_PERM), sp)
+        assert np.array_equal(g.export(X.SRC_OFFSETS), so)
+        if not self_mode:
+            assert np.array_equal(g.export(X.TGT_PERM), tp)
+            assert np.array_equal(g.export(X.TGT_OFFSETS), to)
+        # the sorted coordinates and strengths behind the permutation: through the potentials
+        phi = g.evaluate().cpu().numpy()
+        assert normwise(phi, o.evaluate()) <= TOL
