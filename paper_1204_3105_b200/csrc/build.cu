@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
 // (0..n) writes off[k] = i for prev < k <= cur, prev = sorted[i-1] (-1 at i = 0) and
 // cur = sorted[i] (K+1 at i = n), so every entry is written exactly once
 __global__ void __launch_bounds__(256) k_offsets(const uint32_t* __restrict__ sorted, int64_t n, int64_t K,
-                                                 int32_t* __restrict__ off) {
+                                                 int32_t* __restrict__ off, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   const int64_t prev = i > 0 ? (int64_t)sorted[i - 1] : -1;
@@ -102,7 +103,8 @@ __device__ inline int block_excl_scan(int v, int* total) {
 }
 
 __global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const int32_t* __restrict__ in, int64_t n,
-                                                         int32_t* __restrict__ bsum) {
+                                                         int32_t* __restrict__ bsum, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
   int s = 0;
 #pragma unroll
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const int32_t* __restric
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_block_sums(int32_t* bsum, int64_t nb) {
+__global__ void __launch_bounds__(SCAN_T) k_scan_block_sums(int32_t* bsum, int64_t nb, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   // single block, exclusive scan of up to SCAN_TILE block sums, in place
   int64_t base = threadIdx.x * SCAN_I;
   int v[SCAN_I], s = 0;
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_block_sums(int32_t* bsum, int64
 }
 
 __global__ void __launch_bounds__(SCAN_T) k_scan_apply(const int32_t* in, int64_t n, const int32_t* __restrict__ bsum,
-                                                        int32_t* out) {
+                                                        int32_t* out, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
   int v[SCAN_I], s = 0;
 #pragma unroll
@@ -248,7 +252,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_downsweep(const uint32_t* __rest
 // per tile), counted with shared-memory atomics (the counts do not depend on order)
 __global__ void __launch_bounds__(RS_T) k_radix_count(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                         int db, int32_t* __restrict__ tile_hist, int ntiles,
-                                                        int tile_elems) {
+                                                        int tile_elems, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   __shared__ int cnt[1 << RS_MAXB];
   const int nb = 1 << db;
   const unsigned mask = (unsigned)nb - 1u;
@@ -280,7 +285,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
                                                               int ntiles, uint32_t* __restrict__ keys_out,
                                                               double2* __restrict__ rec_out,
                                                               double2* __restrict__ sxy, double* __restrict__ su,
-                                                              int32_t* __restrict__ perm) {
+                                                              int32_t* __restrict__ perm, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   extern __shared__ double2 rr_smem[];
   double2* srec = rr_smem;                                   // [RR_TILE][2]
   uint32_t* skey = (uint32_t*)(srec + 2 * RR_TILE);          // [RR_TILE]
@@ -411,7 +417,8 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
                                                         const double2* __restrict__ xy,
                                                         const double* __restrict__ u, int64_t n,
                                                         const int32_t* __restrict__ off, int32_t* __restrict__ cur,
-                                                        double2* __restrict__ rec) {
+                                                        double2* __restrict__ rec, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool v = i < n;
   const uint32_t k = v ? key[i] : 0xffffffffu;
@@ -467,7 +474,8 @@ __device__ __forceinline__ void lo_rank_warp(const int* __restrict__ sidx, int n
 
 __global__ void __launch_bounds__(256) k_leaf_order(int64_t nbuckets, const int32_t* __restrict__ off,
                                                     const double2* __restrict__ rec, double2* __restrict__ sxy,
-                                                    double* __restrict__ su, int32_t* __restrict__ perm) {
+                                                    double* __restrict__ su, int32_t* __restrict__ perm, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   __shared__ int sidx[8][LO_WARP_MAX];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t k = blockIdx.x * 8ll + w;
@@ -499,7 +507,8 @@ __global__ void __launch_bounds__(256) k_max_i32(const int32_t* __restrict__ v, 
 
 // (x, y, u, input index) records in input order (the LSD fallback of the bucket sort)
 __global__ void k_make_rec(const double2* __restrict__ xy, const double* __restrict__ u, int64_t n,
-                           double2* __restrict__ rec) {
+                           double2* __restrict__ rec, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   rec[2 * i] = xy[i];
@@ -821,18 +830,24 @@ size_t fmm_scan_scratch_bytes(int64_t n) {
   return (size_t)(nb + 32) * sizeof(int32_t);
 }
 
-int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
-                        cudaStream_t s, int64_t* launches) {
+// gate (device int, optional): the scan runs only when *gate == gate_want (build.cu's sort paths)
+static int device_scan_gated(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
+                             cudaStream_t s, int64_t* launches, const int32_t* gate, int gate_want) {
   if (n <= 0) return FMM_OK;
   int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (nb > SCAN_TILE || scratch_bytes < fmm_scan_scratch_bytes(n)) return FMM_EBADCFG;
   int32_t* bsum = (int32_t*)scratch;
-  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum);
-  k_scan_block_sums<<<1, SCAN_T, 0, s>>>(bsum, nb);
-  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum, out);
+  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum, gate, gate_want);
+  k_scan_block_sums<<<1, SCAN_T, 0, s>>>(bsum, nb, gate, gate_want);
+  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum, out, gate, gate_want);
   *launches += 3;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
+}
+
+int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
+                        cudaStream_t s, int64_t* launches) {
+  return device_scan_gated(in, out, n, scratch, scratch_bytes, s, launches, nullptr, 0);
 }
 
 static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
@@ -910,8 +925,10 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
 // stable LSD radix sort of (key, 32-byte record) pairs of one rank's points: the records move
 // with the keys through every pass and the last pass writes the sorted SoA arrays and the
 // permutation; then the leaf CSR off[0..K+1] from the sorted keys
+// gate (device int, optional): every kernel of the sort runs only when *gate == 1 (the LSD path of
+// single_rank_keys_sort, decided on the device)
 static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2* rec, int64_t n, double2* xy_out,
-                              double* u_out, int32_t* perm, int32_t* off) {
+                              double* u_out, int32_t* perm, int32_t* off, const int32_t* gate = nullptr) {
   cudaStream_t s = t->stream;
   if (n == 0) {
     FMM_CUDA_TRY(cudaMemsetAsync(off, 0, sizeof(int32_t) * (t->g.K + 2), s));
@@ -961,22 +978,22 @@ static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2
     const int64_t nh = ((int64_t)1 << db) * ntiles;
     uint32_t* kout = (ps % 2 == 0) ? kA : kB;
     double2* rout = (ps % 2 == 0) ? rA : rB;
-    k_radix_count<<<ntiles, RS_T, 0, s>>>(kin, n, shift, db, hist, ntiles, RR_TILE);
-    int e = fmm_device_scan_i32(hist, hist, nh, sscr, fmm_scan_scratch_bytes(nh), s, &t->launches);
+    k_radix_count<<<ntiles, RS_T, 0, s>>>(kin, n, shift, db, hist, ntiles, RR_TILE, gate, 1);
+    int e = device_scan_gated(hist, hist, nh, sscr, fmm_scan_scratch_bytes(nh), s, &t->launches, gate, 1);
     if (e) return e;
     if (ps == passes - 1)
       k_radix_scatter_rec<true><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, nullptr,
-                                                              xy_out, u_out, perm);
+                                                              xy_out, u_out, perm, gate, 1);
     else
       k_radix_scatter_rec<false><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, rout,
-                                                               nullptr, nullptr, nullptr);
+                                                               nullptr, nullptr, nullptr, gate, 1);
     t->launches += 2;
     FMM_CUDA_TRY(cudaGetLastError());
     kin = kout;
     rin = rout;
     shift += db;
   }
-  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off, gate, 1);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
@@ -1047,10 +1064,16 @@ static int multi_rank_select(fmm_tree_s* t, uint32_t* ckey, int32_t* cidx, int64
   return FMM_OK;
 }
 
+// mode = 1 (LSD record sort) when some leaf holds more than LO_WARP_MAX points, else 0 (bucket)
+__global__ void k_sort_mode(const int32_t* __restrict__ mx, int32_t* __restrict__ mode) {
+  *mode = *mx > LO_WARP_MAX ? 1 : 0;
+}
+
 // one rank (DESIGN.md §7 "Build"), per point set: the LSD record sort when the leaves hold more
-// than LO_MEAN_MAX points on average; else keys with leaf counts, the leaf CSR from their scan
-// and, when no leaf holds more than LO_WARP_MAX points (one 8-byte read-back), the bucket sort,
-// otherwise the LSD record sort.  FMM_SORT_LSD=1 forces the LSD sort.
+// than LO_MEAN_MAX points on average or the set is small (host decisions); else keys with leaf counts, the leaf CSR
+// from their scan, and both sorts enqueued with every kernel gated by a device mode word -- the
+// bucket sort when no leaf holds more than LO_WARP_MAX points, else the LSD record sort -- so
+// that the build never waits on the device from the host.  FMM_SORT_LSD=1 forces the LSD sort.
 static int single_rank_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
@@ -1063,14 +1086,16 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
   const char* force = getenv("FMM_SORT_LSD");
   const bool force_lsd = force && force[0] == '1';
   bool lsd[2];
-  for (int k = 0; k < 2; ++k) lsd[k] = force_lsd || cnt[k] > LO_MEAN_MAX * K;
-  // scratch per point set: counts (K + 2) | scan scratch; then the two maxima
+  // small point sets (<= 2^20: launch-bound builds) skip the gated pair of paths
+  for (int k = 0; k < 2; ++k) lsd[k] = force_lsd || cnt[k] > LO_MEAN_MAX * K || cnt[k] <= (1 << 20);
+  // scratch per point set: counts (K + 2) | scan scratch; then two maxima and two mode words
   const size_t sscan = fmm_scan_scratch_bytes(nb);
   const size_t hb = ((size_t)nb * 4 + 255) / 256 * 256;
   const size_t per = hb + (sscan + 255) / 256 * 256;
   char* buf = nullptr;
   FMM_CUDA_TRY(cudaMallocAsync((void**)&buf, nsets * per + 256, s));
   int32_t* mx = (int32_t*)(buf + nsets * per);
+  int32_t* mode = mx + 2;
   FMM_CUDA_TRY(cudaMemsetAsync(buf, 0, nsets * per + 256, s));
   auto hist = [&](int k) { return (int32_t*)(buf + k * per); };
   auto sscr = [&](int k) { return (void*)(buf + k * per + hb); };
@@ -1095,39 +1120,32 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
   if (t->timing) cudaEventRecord(t->ev[8], s);
   if (t->timing) cudaEventRecord(t->ev[9], s);
   int e = FMM_OK;
-  bool need_max = false;
-  for (int k = 0; k < nsets && !e; ++k)
-    if (cnt[k] > 0 && !lsd[k]) {
-      e = fmm_device_scan_i32(hist(k), off[k], nb, sscr(k), sscan, s, &t->launches);
-      k_max_i32<<<64, 256, 0, s>>>(hist(k), K + 1, mx + k);
-      t->launches++;
-      need_max = true;
-    }
-  int32_t hmx[2] = {0, 0};
-  if (!e && need_max) {
-    FMM_CUDA_TRY(cudaMemcpyAsync(hmx, mx, sizeof(hmx), cudaMemcpyDeviceToHost, s));
-    FMM_CUDA_TRY(cudaStreamSynchronize(s));
-  }
   for (int k = 0; k < nsets && !e; ++k) {
     if (cnt[k] == 0) {
       FMM_CUDA_TRY(cudaMemsetAsync(off[k], 0, sizeof(int32_t) * nb, s));
       continue;
     }
-    if (!lsd[k] && hmx[k] > LO_WARP_MAX) {  // a large leaf: the LSD sort after all
-      k_make_rec<<<blocks_for(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k]);
-      t->launches++;
-      lsd[k] = true;
-    }
     if (lsd[k]) {
       e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k]);
-    } else {
-      double2* brec = rec[k];  // bucket-ordered records (the input-order records were not needed)
-      int32_t* cur = hist(k);  // the counts, zeroed, become the per-leaf slot cursors
-      FMM_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(int32_t) * nb, s));
-      k_bucket_scatter<<<blocks_for(cnt[k], 256), 256, 0, s>>>(keys[k], xy[k], u[k], cnt[k], off[k], cur, brec);
-      k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], brec, xy_out[k], u_out[k], perm[k]);
-      t->launches += 2;
+      continue;
     }
+    e = fmm_device_scan_i32(hist(k), off[k], nb, sscr(k), sscan, s, &t->launches);
+    if (e) break;
+    k_max_i32<<<64, 256, 0, s>>>(hist(k), K + 1, mx + k);
+    k_sort_mode<<<1, 1, 0, s>>>(mx + k, mode + k);
+    t->launches += 2;
+    // mode 1: input-order records, then the LSD record sort (its offsets overwrite the same CSR)
+    k_make_rec<<<blocks_for(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k], mode + k, 1);
+    t->launches++;
+    e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k], mode + k);
+    if (e) break;
+    // mode 0: the bucket sort; the counts, zeroed, become the per-leaf slot cursors
+    int32_t* cur = hist(k);
+    FMM_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(int32_t) * nb, s));
+    k_bucket_scatter<<<blocks_for(cnt[k], 256), 256, 0, s>>>(keys[k], xy[k], u[k], cnt[k], off[k], cur, rec[k],
+                                                              mode + k, 0);
+    k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], rec[k], xy_out[k], u_out[k], perm[k], mode + k, 0);
+    t->launches += 2;
     FMM_CUDA_TRY(cudaGetLastError());
   }
   for (int k = 0; k < nsets; ++k)
