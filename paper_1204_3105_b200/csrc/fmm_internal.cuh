@@ -137,6 +137,7 @@ int fmm_stage_downward(fmm_tree_s* t);
 int fmm_stage_p2p_pairs(fmm_tree_s* t);
 int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi_out);
 int fmm_build_tasks(fmm_tree_s* t);
+bool fmm_p2p_pairing(const fmm_tree_s* t);  // p2p.cu: TF_PAIR tasks and the pairing kernel variant
 int fmm_stage_gather_strengths(fmm_tree_s* t, const double* u);
 int fmm_debug_p2p_math_launch(const double* dxdy, int64_t n, const double* tabs, double* out, cudaStream_t s);
 // build.cu: the device geometry of a tree (geometry.cuh)

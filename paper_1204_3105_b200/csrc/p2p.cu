@@ -25,6 +25,11 @@ constexpr int P2P_LIGHT = 1 << 16;  // max pairs of one symmetric (single-warp) 
 constexpr int P2P_S = 192;          // sources of one near leaf kept in shared memory per warp
 constexpr int P2P_SD = 320;         // distinct targets: near-list sources kept in shared memory per warp
 constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17, TF_HEAVY = 1 << 18;
+// TF_PAIR (self mode): two light off-diagonal blocks (t, s1), (t, s2) of one row leaf in one task,
+// the columns s1's sources then s2's (<= P2P_S together, staged once):
+// y = q1 | q1r << 8 | flags | q2 << 20 | q2r << 24 (FMM_NEAR_MAX = 16); the row sums go to slot q1
+// and slot q2 of every row receives 0.  Only the staging and the task's last writes read them.
+constexpr int TF_PAIR = 1 << 19;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -34,11 +39,13 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
 __device__ __forceinline__ int split_rows(int ns) { return max(8, (P2P_LIGHT / max(ns, 1)) & ~7); }
 
 // tasks of target leaf t: count (out == nullptr) or write them from *pos
+// mode: bit 0 = self mode, bit 1 = TF_PAIR tasks allowed (the pairing kernel variant runs)
 __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
-                          const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int self_mode,
+                          const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int mode,
                           int64_t lo, int64_t hi, int4* out) {
   const int nt = toff[t + 1] - toff[t];
   if (nt == 0) return 0;
+  const bool self_mode = mode & 1, pairs = (mode >> 1) & 1;
   const bool t_in = t >= lo && t < hi;
   const int nn = nnear[t];
   int c = 0;
@@ -51,6 +58,13 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
       const int s = near[(int64_t)a.x * FMM_NEAR_MAX + (a.y & 0xff)];
       out[2 * c] = a;
       out[2 * c + 1] = make_int4(toff[a.x], soff[s], ncols, s);
+    }
+    ++c;
+  };
+  auto put_pair = [&](int q1, int q1r, int q2, int q2r) {
+    if (out) {
+      out[2 * c] = make_int4(t, q1 | (q1r << 8) | TF_SYM | TF_PAIR | (q2 << 20) | (q2r << 24), 0, nt);
+      out[2 * c + 1] = make_int4(0, 0, 0, 0);
     }
     ++c;
   };
@@ -70,6 +84,8 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
     if (tot > 0) emit_rows(t, 0, nt, tot, 0);
     return c;
   }
+  // a light block of an own row leaf waiting for a partner (TF_PAIR): slot, reverse slot, sources
+  int pq = -1, pqr = 0, pns = 0;
   for (int q = 0; q < nn; ++q) {
     const int s = near[(int64_t)t * FMM_NEAR_MAX + q];
     const int ns = soff[s + 1] - soff[s];
@@ -92,7 +108,18 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
     for (int k = 0; k < nnear[s]; ++k)
       if (near[(int64_t)s * FMM_NEAR_MAX + k] == t) qr = k;
     if ((int64_t)nt * ns <= P2P_LIGHT) {
-      if (t_in || s_in) {
+      if (pairs && t_in && ns <= P2P_S) {
+        // paired with the previous light block of t when both column leaves fit shared memory
+        if (pq >= 0 && pns + ns <= P2P_S) {
+          put_pair(pq, pqr, q, qr);
+          pq = -1;
+        } else {
+          if (pq >= 0) put(make_int4(t, pq | (pqr << 8) | TF_SYM, 0, nt), pns);
+          pq = q;
+          pqr = qr;
+          pns = ns;
+        }
+      } else if (t_in || s_in) {
         put(make_int4(t, q | (qr << 8) | TF_SYM, 0, nt), ns);
       }
     } else if (t_in || s_in) {
@@ -104,6 +131,7 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
                 TF_SYM | TF_HEAVY);
     }
   }
+  if (pq >= 0) put(make_int4(t, pq | (pqr << 8) | TF_SYM, 0, nt), pns);
   return c;
 }
 
@@ -200,9 +228,56 @@ __device__ __noinline__ PairOut p2p_slow(double dx, double dy, double r2, bool s
   return o;
 }
 
+// TF_PAIR staging: s1's sources [sb, sb + n1) then s2's into s_xy / s_u (padded to a multiple of
+// 32), reactions zeroed; returns the column count.
+__device__ __forceinline__ int p2p_stage_pair(int ty, int t, int sb, int n1, const int32_t* __restrict__ soff,
+                                              const int32_t* __restrict__ near, const double2* __restrict__ sxy,
+                                              const double* __restrict__ su, double2* s_xy, double* s_u,
+                                              double2* s_re) {
+  const int lane = threadIdx.x & 31;
+  const int s2 = near[(int64_t)t * FMM_NEAR_MAX + ((ty >> 20) & 15)];
+  const int sb2 = soff[s2], ns = n1 + soff[s2 + 1] - sb2;
+  for (int i = lane; i < ((ns + 31) & ~31); i += 32) {
+    if (i < ns) {
+      const int j = i < n1 ? sb + i : sb2 + (i - n1);
+      s_xy[i] = sxy[j];
+      s_u[i] = su[j];
+    } else {
+      s_xy[i] = make_double2(-P2P_PAD, P2P_PAD);
+      s_u[i] = 0.0;
+    }
+    s_re[i] = make_double2(0.0, 0.0);
+  }
+  __syncwarp();
+  return ns;
+}
+
+// TF_PAIR last writes: the two column leaves' reactions to their reverse slots, 0 to slot q2 of
+// every row
+__device__ __forceinline__ void p2p_finish_pair(int ty, int t, int tb, int nrows, int sb, int qr, int ns,
+                                                bool write_rows, bool write_react, int64_t lo, int64_t hi,
+                                                const int32_t* __restrict__ soff, const int32_t* __restrict__ near,
+                                                const double2* s_re, double2* __restrict__ part, int nslot) {
+  const int lane = threadIdx.x & 31;
+  const int s1 = near[(int64_t)t * FMM_NEAR_MAX + (ty & 0xff)];
+  const int n1 = soff[s1 + 1] - soff[s1], q2 = (ty >> 20) & 15, q2r = (ty >> 24) & 15;
+  const int s2 = near[(int64_t)t * FMM_NEAR_MAX + q2], sb2 = soff[s2];
+  const bool write_react2 = s2 >= lo && s2 < hi;
+  for (int i = lane; i < ns; i += 32) {
+    if (i < n1) {
+      if (write_react) part[(int64_t)(sb + i) * nslot + qr] = s_re[i];
+    } else if (write_react2) {
+      part[(int64_t)(sb2 + i - n1) * nslot + q2r] = s_re[i];
+    }
+  }
+  if (write_rows)
+    for (int i = lane; i < nrows; i += 32) part[(int64_t)(tb + i) * nslot + q2] = make_double2(0.0, 0.0);
+}
+
 // SELF: self mode (symmetric tasks possible); the distinct-target instantiation has no
 // reversed-pair work at all
-template <bool SELF>
+// PAIRS: the variant that runs TF_PAIR tasks (self mode; fmm_p2p_pairing decides)
+template <bool SELF, bool PAIRS>
 __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
     const int4* __restrict__ tasks, const int32_t* __restrict__ ntask_p, int32_t* __restrict__ next_task,
     const int32_t* __restrict__ toff, const int32_t* __restrict__ soff, const double2* __restrict__ txy,
@@ -287,6 +362,8 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
         s_u[i] = 0.0;
       }
       __syncwarp();
+    } else if (PAIRS && (tk.y & TF_PAIR)) {
+      ns = p2p_stage_pair(tk.y, t, sb, ns, soff, near, sxy, su, s_xy, s_u, s_re);
     } else if (whole) {
       for (int i = lane; i < ((ns + 31) & ~31); i += 32) {
         if (i < ns) {
@@ -497,7 +574,9 @@ __global__ void __launch_bounds__(32 * P2P_WARPS, P2P_MINB) k_p2p_pairs(
       __syncwarp();
     }
     __syncwarp();
-    if (whole && write_react) {
+    if (PAIRS && (tk.y & TF_PAIR)) {
+      p2p_finish_pair(tk.y, t, tb, tk.w, sb, qr, ns, write_rows, write_react, lo, hi, soff, near, s_re, part, nslot);
+    } else if (whole && write_react) {
       if (heavy) {
         for (int i = lane; i < ns; i += 32) {
           double2* slot = part + (int64_t)(sb + i) * nslot + qr;
@@ -634,19 +713,33 @@ __global__ void k_debug_p2p_math(const double2* __restrict__ d, int64_t n, const
 
 }  // namespace
 
+// Pairing of light off-diagonal blocks (TF_PAIR, self mode) pays where leaves average 32-96
+// points on a tree of > 2^20 points (column padding and row-step heads halved: C4q -3 %, C4t
+// -4 %); elsewhere the pairing
+// variant of the kernel only costs (its larger code shifts the register allocation: C4s +2.4 %
+// with no pair formed, C5 +1.4 %), so those trees keep the plain kernel.  FMM_P2P_PAIRS=0 / 1
+// overrides.
+bool fmm_p2p_pairing(const fmm_tree_s* t) {
+  if (!t->g.self_mode) return false;
+  const char* f = getenv("FMM_P2P_PAIRS");
+  if (f && (f[0] == '0' || f[0] == '1')) return f[0] == '1';
+  const double mean = (double)t->n / (double)t->g.K;
+  return t->n > (1 << 20) && mean >= 32.0 && mean <= 96.0;  // small trees: too few tasks (C2 +16 %)
+}
+
 int fmm_build_tasks(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const int64_t K = t->g.K;
+  const int mode = (t->g.self_mode ? 1 : 0) | (fmm_p2p_pairing(t) ? 2 : 0);
   int32_t* cnt = nullptr;
   size_t sb = fmm_scan_scratch_bytes(K + 1);
   FMM_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (K + 1) + sb, s));
-  k_task_count<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear,
-                                                                t->g.self_mode, t->leaf_lo, t->leaf_hi, cnt);
+  k_task_count<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear, mode,
+                                                                t->leaf_lo, t->leaf_hi, cnt);
   int e = fmm_device_scan_i32(cnt, cnt, K + 1, cnt + K + 1, sb, s, &t->launches);
   if (!e)
-    k_task_fill<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear,
-                                                                 t->g.self_mode, t->leaf_lo, t->leaf_hi, cnt,
-                                                                 t->tasks, t->ntask);
+    k_task_fill<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear, mode,
+                                                                 t->leaf_lo, t->leaf_hi, cnt, t->tasks, t->ntask);
   t->launches += 2;
   cudaFreeAsync(cnt, s);
   FMM_CUDA_TRY(cudaGetLastError());
@@ -670,7 +763,8 @@ int fmm_stage_p2p_pairs(fmm_tree_s* t) {
                                                            t->status);
     return FMM_OK;
   };
-  int e = G.self_mode ? launch(k_p2p_pairs<true>) : launch(k_p2p_pairs<false>);
+  int e = !G.self_mode ? launch(k_p2p_pairs<false, false>)
+                       : (fmm_p2p_pairing(t) ? launch(k_p2p_pairs<true, true>) : launch(k_p2p_pairs<true, false>));
   if (e) return e;
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());

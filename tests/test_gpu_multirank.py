@@ -196,3 +196,15 @@ def test_single_rank_comm_allreduce_path():
     finally:
         comm.close()
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4ts"])
+def test_multirank_with_pairing(name, monkeypatch):
+    """Ranks 0..2 with the pairing kernel variant forced (TF_PAIR tasks are formed for own row
+    leaves only; their two column leaves may belong to other ranks): the union equals the oracle."""
+    monkeypatch.setenv("FMM_P2P_PAIRS", "1")
+    w = CASES[name]
+    d = data(w)
+    phi, _, _ = run_ranks(w, d, 3)
+    assert not np.isnan(phi).any(), "a target was written by no rank"
+    assert normwise(phi, oracle_phi(name)) <= TOL

@@ -345,3 +345,21 @@ def test_sort_paths_bit_exact(case, monkeypatch):
                 assert normwise(phi, ref) <= 1e-14
             else:
                 assert np.array_equal(phi.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("pairs", ["1", "0"])
+@pytest.mark.parametrize("name", ["C2", "C4qs", "C4ts", "C4ss", "C5s"])
+def test_p2p_pairing_variants(name, pairs, monkeypatch):
+    """Both pair-kernel variants (p2p.cu fmm_p2p_pairing: TF_PAIR tasks -- two light off-diagonal
+    near leaves of a row leaf in one task -- and the plain kernel), forced by FMM_P2P_PAIRS, on
+    every tiling and the clustered case against the oracle (D15), and bitwise repeatable.  The
+    scaled-down cases have fewer points per leaf than the benchmark trees, so the default rule
+    would not pair them."""
+    monkeypatch.setenv("FMM_P2P_PAIRS", pairs)
+    w = SMALL_CASES[name]
+    d = data(w)
+    g = gpu_tree(w, d)
+    phi = g.evaluate().cpu().numpy()
+    g.check()
+    assert normwise(phi, oracle_tree(w, d).evaluate()) <= TOL
+    assert np.array_equal(phi, g.evaluate().cpu().numpy()) or name == "C5s"  # C5s: heavy blocks (atomics)
