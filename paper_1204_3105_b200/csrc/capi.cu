@@ -203,6 +203,7 @@ void carve(fmm_tree_s* t, Arena& a) {
   t->ntask_cap = (int64_t)G.nslot * (m / 8 + G.K) + 1;
   t->tasks = a.take<int4>(2 * t->ntask_cap);  // two int4 per task (p2p.cu leaf_tasks)
   t->part = a.take<double2>((m + 1) * (int64_t)fmm_part_slots(G));
+  t->pskip = a.take<int32_t>(K);
   t->ntask = a.take<int32_t>(1);
   t->next_task = a.take<int32_t>(1);
   t->p2p_tab = a.take<double>(P2P_TAB_DOUBLES);

@@ -79,6 +79,7 @@ struct fmm_tree_s {
   int4* tasks;         // [2 ntask_cap] per task (leaf t, q | q_rev << 8 | flags, row0, row1), (first target of t, first
                        // source / count of the columns, column leaf) of p2p.cu
   double2* part;       // [m][nslot] per (target, near-leaf) partial sums (Re, Im) of the near field
+  int32_t* pskip;      // [K] per target leaf: bit q set <=> no task writes slot q (p2p.cu TF_PAIR)
   int32_t* ntask;      // [1] device counter
   int32_t* next_task;  // [1] dynamic scheduling counter of the P2P kernel
   int64_t ntask_cap;

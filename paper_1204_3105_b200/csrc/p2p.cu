@@ -27,8 +27,9 @@ constexpr int P2P_SD = 320;         // distinct targets: near-list sources kept 
 constexpr int TF_SYM = 1 << 16, TF_DIAG = 1 << 17, TF_HEAVY = 1 << 18;
 // TF_PAIR (self mode): two light off-diagonal blocks (t, s1), (t, s2) of one row leaf in one task,
 // the columns s1's sources then s2's (<= P2P_S together, staged once):
-// y = q1 | q1r << 8 | flags | q2 << 20 | q2r << 24 (FMM_NEAR_MAX = 16); the row sums go to slot q1
-// and slot q2 of every row receives 0.  Only the staging and the task's last writes read them.
+// y = q1 | q1r << 8 | flags | q2 << 20 | q2r << 24 (FMM_NEAR_MAX = 16); the row sums go to slot q1,
+// slot q2 of the rows is never written and the finish skips it (pskip).  Only the staging and the
+// task's last writes read the pair fields.
 constexpr int TF_PAIR = 1 << 19;
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
@@ -40,9 +41,11 @@ __device__ __forceinline__ int split_rows(int ns) { return max(8, (P2P_LIGHT / m
 
 // tasks of target leaf t: count (out == nullptr) or write them from *pos
 // mode: bit 0 = self mode, bit 1 = TF_PAIR tasks allowed (the pairing kernel variant runs)
+// skip (optional): the slots of t's targets no task writes (slot q2 of every TF_PAIR task)
 __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
                           const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int mode,
-                          int64_t lo, int64_t hi, int4* out) {
+                          int64_t lo, int64_t hi, int4* out, int32_t* skip = nullptr) {
+  if (skip) *skip = 0;
   const int nt = toff[t + 1] - toff[t];
   if (nt == 0) return 0;
   const bool self_mode = mode & 1, pairs = (mode >> 1) & 1;
@@ -66,6 +69,7 @@ __device__ int leaf_tasks(int t, const int32_t* __restrict__ toff, const int32_t
       out[2 * c] = make_int4(t, q1 | (q1r << 8) | TF_SYM | TF_PAIR | (q2 << 20) | (q2r << 24), 0, nt);
       out[2 * c + 1] = make_int4(0, 0, 0, 0);
     }
+    if (skip) *skip |= 1 << q2;
     ++c;
   };
   auto emit_rows = [&](int leaf, int qq, int rows, int ns, int flags) {
@@ -159,14 +163,14 @@ __global__ void k_task_count(int64_t K, const int32_t* __restrict__ toff, const 
 __global__ void k_task_fill(int64_t K, const int32_t* __restrict__ toff, const int32_t* __restrict__ soff,
                             const int32_t* __restrict__ near, const int32_t* __restrict__ nnear, int self_mode,
                             int64_t lo, int64_t hi, const int32_t* __restrict__ start, int4* __restrict__ tasks,
-                            int32_t* __restrict__ ntask) {
+                            int32_t* __restrict__ ntask, int32_t* __restrict__ pskip) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t > K) return;
   if (t == K) {
     *ntask = start[K];
     return;
   }
-  leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, tasks + 2 * (int64_t)start[t]);
+  leaf_tasks((int)t, toff, soff, near, nnear, self_mode, lo, hi, tasks + 2 * (int64_t)start[t], pskip + t);
 }
 
 // ------------------------------------------------------------------ the pair kernel
@@ -252,8 +256,8 @@ __device__ __forceinline__ int p2p_stage_pair(int ty, int t, int sb, int n1, con
   return ns;
 }
 
-// TF_PAIR last writes: the two column leaves' reactions to their reverse slots, 0 to slot q2 of
-// every row
+// TF_PAIR last writes: the two column leaves' reactions to their reverse slots (slot q2 of the rows
+// stays unwritten: the finish skips it, pskip)
 __device__ __forceinline__ void p2p_finish_pair(int ty, int t, int tb, int nrows, int sb, int qr, int ns,
                                                 bool write_rows, bool write_react, int64_t lo, int64_t hi,
                                                 const int32_t* __restrict__ soff, const int32_t* __restrict__ near,
@@ -270,8 +274,9 @@ __device__ __forceinline__ void p2p_finish_pair(int ty, int t, int tb, int nrows
       part[(int64_t)(sb2 + i - n1) * nslot + q2r] = s_re[i];
     }
   }
-  if (write_rows)
-    for (int i = lane; i < nrows; i += 32) part[(int64_t)(tb + i) * nslot + q2] = make_double2(0.0, 0.0);
+  (void)write_rows;
+  (void)tb;
+  (void)nrows;
 }
 
 // SELF: self mode (symmetric tasks possible); the distinct-target instantiation has no
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
                                                     const double2* __restrict__ loc_leaf, int p,
                                                     const int32_t* __restrict__ tperm,
                                                     const double2* __restrict__ part, int nslot,
-                                                    double2* __restrict__ phi) {
+                                                    const int32_t* __restrict__ pskip, double2* __restrict__ phi) {
   __shared__ double2 s_loc[4][32];
   const int64_t t = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -609,6 +614,7 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
   const int tb = toff[t], nt = toff[t + 1] - tb;
   if (nt == 0) return;
   const int nn = nnear[t];
+  const unsigned skip = (unsigned)pskip[t];  // slots no task writes (TF_PAIR's q2): read as 0
   const double2 c = cen_leaf[t];
   // the leaf's local expansion in shared memory (one coalesced load), so that the Horner
   // steps below do not wait on a global load each
@@ -619,7 +625,8 @@ __global__ void __launch_bounds__(128) k_p2p_finish(int64_t lo, int64_t hi, cons
     const int tpos = tb + i;
     double2 v[NS];
 #pragma unroll
-    for (int q = 0; q < NS; ++q) v[q] = q < nn ? part[(int64_t)tpos * nslot + q] : make_double2(0.0, 0.0);
+    for (int q = 0; q < NS; ++q)
+      v[q] = (q < nn && !((skip >> q) & 1u)) ? part[(int64_t)tpos * nslot + q] : make_double2(0.0, 0.0);
     double re = 0.0, im = 0.0;
 #pragma unroll
     for (int q = 0; q < NS; ++q) {  // near-list order
@@ -740,7 +747,8 @@ int fmm_build_tasks(fmm_tree_s* t) {
   int e = fmm_device_scan_i32(cnt, cnt, K + 1, cnt + K + 1, sb, s, &t->launches);
   if (!e)
     k_task_fill<<<(unsigned)((K + 1 + 255) / 256), 256, 0, s>>>(K, t->toff, t->soff, t->near, t->nnear, mode,
-                                                                 t->leaf_lo, t->leaf_hi, cnt, t->tasks, t->ntask);
+                                                                 t->leaf_lo, t->leaf_hi, cnt, t->tasks, t->ntask,
+                                                                 t->pskip);
   t->launches += 2;
   cudaFreeAsync(cnt, s);
   FMM_CUDA_TRY(cudaGetLastError());
@@ -782,7 +790,7 @@ int fmm_stage_p2p_finish(fmm_tree_s* t, double2* phi) {
   case NS:                                                                                                    \
     k_p2p_finish<NS><<<(unsigned)((nl * 32 + 127) / 128), 128, 0, s>>>(                                       \
         t->leaf_lo, t->leaf_hi, t->toff, t->nnear, t->txy, t->centre + G.lvl_off[G.L],                        \
-        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, NS, phi);                                  \
+        t->loc + G.lvl_off[G.L] * (G.p + 1), G.p, t->tperm, t->part, NS, t->pskip, phi);                        \
     break;
       FMM_FINISH(1)
       FMM_FINISH(7)
