@@ -72,7 +72,9 @@ int fmm_nccl_version(void);
  *                 is the island of the 7^L leaf hexagons (reading D8).
  *   FMM_TRIQUAD : root_x, root_y = centroid of the upright root triangle; root_size = its
  *                 circumradius R0 (level-l circumradius R0 * 2^-l).
- * depth  L: quadtree / triangle 1..15, septree 1..10 (leaf keys must fit 32 bits).
+ * depth  L: quadtree / triangle 1..12, septree 1..9 for fmm_build_tree (the K + 2 leaf counts
+ *           must fit one device scan of 8192^2 entries); the geometry-only calls
+ *           (fmm_sample_cells) accept quadtree / triangle 1..15, septree 1..10 (32-bit keys).
  *           |root_x| + 2 root_size and |root_y| + 2 root_size must be < 1e20 (the P2P kernel
  *           pads with points at 1e30), root_size > 0, all finite; else FMM_EBADCFG.
  * p       : expansion terms, 1..31 (multipole Q, a_1..a_p; local b_0..b_p).
@@ -109,8 +111,11 @@ typedef struct {
 typedef struct fmm_tree_s* fmm_tree_t;
 
 /* Build the tree: leaf keys (CellIndex, P:207-250 / P:342-364 / Morton), a stable
- * radix sort of points by (leaf key, input index), leaf CSR offsets, cell centres
- * (CellCenter, bit-exact lattice form D12) and the near / E4 interaction lists.
+ * sort of points by (leaf key, input index) -- a bucket sort for small leaves, else an LSD
+ * radix sort --, leaf CSR offsets, cell centres (CellCenter, bit-exact
+ * lattice form D12), the near / E4 interaction lists and the near-field task list.
+ * n, m <= 2^27 and the depth limits of fmm_config, else FMM_EBADCFG with a message
+ * (fmm_last_error_message).
  *
  * src_xy: n points as interleaved (x, y) float64 pairs (complex128 layout);
  * src_u : n real float64 strengths; tgt_xy: m points (ignored, may be NULL, in

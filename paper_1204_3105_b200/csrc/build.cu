@@ -850,6 +850,8 @@ int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratc
   return device_scan_gated(in, out, n, scratch, scratch_bytes, s, launches, nullptr, 0);
 }
 
+int64_t fmm_scan_max_entries() { return (int64_t)SCAN_TILE * SCAN_TILE; }
+
 static int key_bits(int64_t K) {  // keys are 0..K (K = sentinel)
   int b = 1;
   while (((int64_t)1 << b) <= K) ++b;

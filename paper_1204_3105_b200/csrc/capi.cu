@@ -387,7 +387,16 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   Geo g;
   int e = make_geo(cfg, &g);
   if (e) return e;
-  if (n < 0 || m < 0 || n >= ((int64_t)1 << 31) - 64 || m >= ((int64_t)1 << 31) - 64) return FMM_EBADCFG;
+  if (n < 0 || m < 0) return FMM_EBADCFG;
+  // limits of the build's device scans (leaf counts, task counts, radix digit histograms)
+  if (g.K + 2 > fmm_scan_max_entries()) {
+    fmm_set_error_message("depth too large for the build: at most 12 (quadtree, triangle) or 9 (septree) levels");
+    return FMM_EBADCFG;
+  }
+  if (n > FMM_MAX_POINTS || m > FMM_MAX_POINTS) {
+    fmm_set_error_message("too many points: at most 2^27 sources and 2^27 targets per tree");
+    return FMM_EBADCFG;
+  }
   if (cfg->self_mode) {
     if (m != n && m != 0 && tgt_xy) return FMM_EBADCFG;
     m = n;

@@ -132,6 +132,10 @@ int32_t fmm_comm_rank(fmm_comm_t c);
 int fmm_device_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, size_t scratch_bytes,
                         cudaStream_t s, int64_t* launches);
 size_t fmm_scan_scratch_bytes(int64_t n);
+int64_t fmm_scan_max_entries();  // largest input of fmm_device_scan_i32 (8192^2)
+// the build's limits from its device scans (fmm_build_tree checks them up front): the K + 2 leaf
+// counts and the radix digit histograms (1024 per 2048-point tile) must fit one scan
+constexpr int64_t FMM_MAX_POINTS = (int64_t)1 << 27;
 // passes.cu
 int fmm_stage_upward(fmm_tree_s* t);
 int fmm_stage_downward(fmm_tree_s* t);

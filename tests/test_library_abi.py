@@ -60,3 +60,24 @@ def test_product_package_does_not_touch_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "fmm_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_build_limits_refused_up_front():
+    """Depths and point counts beyond the build's device scans are refused before any CUDA call
+    with FMM_EBADCFG and a message (no GPU needed: the checks precede the device work)."""
+    import ctypes as C
+
+    from paper_1204_3105_b200 import Config, lib
+
+    L = lib()
+    L.fmm_build_tree.restype = C.c_int
+    L.fmm_last_error_message.restype = C.c_char_p
+    for tiling, depth, n in (("quad", 13, 16), ("sept", 10, 16), ("triq", 12, (1 << 27) + 1)):
+        cfg = Config.make(tiling, depth, 8, 0.0, 0.0, 1.0, True)
+        out = C.c_void_p()
+        xy = (C.c_double * 2)()
+        u = (C.c_double * 1)()
+        rc = L.fmm_build_tree(C.byref(cfg), xy, u, C.c_int64(n), None, C.c_int64(0), None, C.byref(out))
+        assert rc == 1 and not out.value, (tiling, depth, rc)  # FMM_EBADCFG
+        msg = L.fmm_last_error_message().decode()
+        assert ("depth" in msg) if n < (1 << 27) else ("points" in msg), msg
