@@ -329,10 +329,15 @@ int fmm_stage_upward(fmm_tree_s* t) {
 // M2L in the Pascal-scaled form: for a batch of NB sources s of E4(t),
 //   Y[l][s] = sum_{k=1..p} C(l+k-1, k-1) a~_{s,k},   a~_{s,k} = (-1)^k a_{s,k} w_s^k,
 //   b_l += w_s^l (Y[l][s] - Q_s / l)   (l >= 1),     b_0 += Q_s Log(c_t - c_s) + Y[0][s]
-// The contraction Y = Cb * A~ (Cb: (p+1) x p real, stored as (-1)^k C(l+k-1, k-1) so that the
-// staged A~ is a_{s,k} w_s^k without the sign; A~: p x 2 NB, real and imaginary parts as
-// columns) runs on DMMA (mma.sync m8n8k4 f64, IEEE FP64 multiply-adds): Cb lives in the A
-// fragments of the warp's registers, A~ is staged in shared memory.  Fragment layouts
+// The contraction Y = Cb * A~ over the rows l = 1..p (Cb: p x p real, stored as
+// (-1)^k C(l+k-1, k-1) so that the staged A~ is a_{s,k} w_s^k without the sign; A~: p x 2 NB, real
+// and imaginary parts as columns) runs on DMMA (mma.sync m8n8k4 f64, IEEE FP64 multiply-adds): Cb
+// lives in the A fragments of the warp's registers, A~ is staged in shared memory.  Row l = 0 has
+// C(k-1, k-1) = 1: Y[0][s] is the plain sum of the a~_{s,k}; when P is a multiple of 8 the staging
+// lanes form it (ROW0) and the row tiles cover l = 1..P, so that p = 24 (16) needs 3 (2) row tiles
+// of 8 instead of 4 (3); otherwise row 0 rides in the first tile for free.  b_0's Q_s Log(c_t - c_s)
+// terms are formed before the batch loop with one source per lane (inside the loop only the 8
+// lanes j = 0 would run the ~70-instruction Log, once per batch).  Fragment layouts
 // (m8n8k4 .f64): A[r][c] at lane 4r + c; B[k][n] at lane 4n + k; C[r][2c + {0,1}] at lane 4r + c.
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -341,13 +346,15 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 // shared memory of one k_down_mma block (dynamic): P2P log / atan tables (b_0's Log), the
-// binomial A fragments, then per warp: powers, a~, Log, L2L part, Q, source ids
+// binomial A fragments, then per warp: powers, a~, L2L part, Q, source ids
 template <int P>
 struct DownSmem {
-  static constexpr int NB = 8, MT = (P + 8) / 8, KT = P / 4;
+  static constexpr bool ROW0 = P % 8 == 0;  // row l = 0 formed outside the DMMA tiles
+  static constexpr int R0 = ROW0 ? 1 : 0;   // first row of the tiles
+  static constexpr int NB = 8, MT = ROW0 ? P / 8 : (P + 8) / 8, KT = P / 4;  // rows R0 .. R0 + 8 MT - 1
   static constexpr size_t tab = sizeof(double2) * (P2P_LOGC_N + 8 * (P2P_ATAN_K + 1));
-  static constexpr size_t afr = sizeof(double) * (MT * KT * 32 + 8 * MT);  // + 1/r table
-  static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + NB + 32) + sizeof(double) * NB +
+  static constexpr size_t afr = sizeof(double) * (MT * KT * 32 + 8 * MT + 8);  // + 1/r table, r = 0..8 MT
+  static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + 32) + sizeof(double) * NB +
                                  sizeof(int) * FMM_CAND_MAX;
   static constexpr size_t bytes = tab + afr + 4 * warp;
 };
@@ -369,7 +376,8 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
                                                      const double* __restrict__ binom, const double* __restrict__ tabs,
                                                      double2* __restrict__ loc_l) {
   using S = DownSmem<P>;
-  constexpr int NB = S::NB, MT = S::MT, KT = S::KT;
+  constexpr int NB = S::NB, MT = S::MT, KT = S::KT, R0 = S::R0;
+  constexpr bool ROW0 = S::ROW0;
   extern __shared__ double2 dsm[];
   double2* s_log = dsm;
   double2* s_atan = s_log + P2P_LOGC_N;
@@ -378,21 +386,20 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   char* wb = (char*)dsm + S::tab + S::afr + w * S::warp;
   double2* s_pw = (double2*)wb;          // [NB][P+1] w_s^k
   double2* s_at = s_pw + NB * (P + 1);   // [NB][P]   a~_{s,k}, k = 1..P
-  double2* s_lg = s_at + NB * P;         // [NB]      Log(c_t - c_s)
-  double2* s_b = s_lg + NB;              // [32]      L2L part
+  double2* s_b = s_at + NB * P;          // [32]      L2L part
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
   p2p_load_tables_compact(tabs, s_log, s_atan);  // ends with __syncthreads
-  // A fragments: Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in), row r = 8 mt + ln/4,
+  // A fragments: Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in), row r = 8 mt + ln/4 + R0,
   // column k = 4 kt + ln%4 + 1
   for (int i = threadIdx.x; i < MT * KT * 32; i += blockDim.x) {
     const int ln = i & 31, kt = (i >> 5) % KT, mt = (i >> 5) / KT;
-    const int r = 8 * mt + (ln >> 2), k = 4 * kt + (ln & 3) + 1;
+    const int r = 8 * mt + (ln >> 2) + R0, k = 4 * kt + (ln & 3) + 1;
     const double c = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
     s_afr[i] = (k & 1) ? -c : c;
   }
-  double* s_invr = s_afr + MT * KT * 32;  // [8 MT] 1/r (0 for r = 0)
-  for (int i = threadIdx.x; i < 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
+  double* s_invr = s_afr + MT * KT * 32;  // [8 MT + 1] 1/r (0 for r = 0)
+  for (int i = threadIdx.x; i <= 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
   __syncthreads();
   const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
   const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // cells [cell0, ncells)
@@ -432,15 +439,28 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt] = make_double2(0.0, 0.0);
   __syncwarp();
-  for (int b0 = 0; b0 < nsrc; b0 += NB) {
-    const int nb = min(NB, nsrc - b0);
+  // ---- b_0 of the M2L, partial per lane: Q_s Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero;
+  // table-driven), one source per lane; ROW0 adds the Y[0][s] of the staging lanes j = 0 below
+  double2 b0 = make_double2(0.0, 0.0);
+  for (int i = lane; i < nsrc; i += 32) {
+    const int src = s_src[i];
+    const double2 cs = cen_l[src];
+    const double Q = mp_l[(int64_t)src * (p + 1)].x;
+    const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
+    b0.x = fma(Q, 0.5 * p2p_log<P2P_LOGC_N>(fma(dx, dx, dy * dy), a_log), b0.x);
+    b0.y = fma(Q, p2p_atan2<false>(dy, dx, a_atan), b0.y);
+  }
+  for (int b0s = 0; b0s < nsrc; b0s += NB) {
+    const int nb = min(NB, nsrc - b0s);
     // lane = (source s = lane / 4, residue j = lane % 4) owns exponents k = 4m + j: it loads
-    // a_{s,k} (all its loads first), forms w^k and a_{s,k} w^k (the (-1)^k of a~ is in Cb)
+    // a_{s,k} (all its loads first), forms w^k and a_{s,k} w^k (the (-1)^k of a~ is in Cb) and
+    // (ROW0) its share of Y[0][s] = sum_k (-1)^k a_{s,k} w^k ((-1)^k = (-1)^j)
     {
       constexpr int NM = P / 4 + 1;
       const int s = lane >> 2, j = lane & 3;
+      double2 y0 = make_double2(0.0, 0.0);
       if (s < nb) {
-        const int src = s_src[b0 + s];
+        const int src = s_src[b0s + s];
         const double2* ab = mp_l + (int64_t)src * (p + 1);
         double2 av[NM];
 #pragma unroll
@@ -456,13 +476,22 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
         for (int m = 0; m < NM; ++m) {
           const int k = 4 * m + j;
           if (k <= P) s_pw[s * (P + 1) + k] = pw;
-          if (k >= 1 && k <= P) s_at[s * P + k - 1] = cmul(av[m], pw);  // (-1)^k is in Cb
+          if (k >= 1 && k <= P) {
+            const double2 at = cmul(av[m], pw);  // (-1)^k is in Cb
+            s_at[s * P + k - 1] = at;
+            if (ROW0) y0 = cadd(y0, at);
+          }
           pw = cmul(pw, w4);
         }
-        if (j == 0) {  // Log(c_t - c_s) (D13 iii; canonical +0 imaginary zero), table-driven
-          const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
-          s_lg[s] = make_double2(0.5 * p2p_log<P2P_LOGC_N>(fma(dx, dx, dy * dy), a_log), p2p_atan2<false>(dy, dx, a_atan));
-          s_q[s] = av[0].x;
+        if (j == 0) s_q[s] = av[0].x;
+      }
+      if (ROW0) {  // every lane's share, signed (lanes past nb carry 0): the final sum over lanes adds them
+        if (j & 1) {
+          b0.x -= y0.x;
+          b0.y -= y0.y;
+        } else {
+          b0.x += y0.x;
+          b0.y += y0.y;
         }
       }
     }
@@ -482,18 +511,17 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) dmma884(d[mt][0], d[mt][1], s_afr[(mt * KT + kt) * 32 + lane], bfr);
       }
-      // C[r][2c + {0,1}] at lane 4r + c: row r = l, source s = 4 nt + lane % 4 (re, im)
+      // C[r][2c + {0,1}] at lane 4r + c: row l = 8 mt + lane / 4 + R0, source s = 4 nt + lane % 4 (re, im)
       const int s = 4 * nt + (lane & 3);
       if (s < nb) {
         const double Q = s_q[s];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const int r = 8 * mt + (lane >> 2);
+          const int r = 8 * mt + (lane >> 2) + R0;
           if (r > P) continue;
-          if (r == 0) {
-            const double2 lg = s_lg[s];
-            acc[mt].x += Q * lg.x + d[mt][0];
-            acc[mt].y += Q * lg.y + d[mt][1];
+          if (!ROW0 && r == 0) {  // Y[0][s] (w^0 = 1; Q_s Log is in b0)
+            acc[mt].x += d[mt][0];
+            acc[mt].y += d[mt][1];
           } else {
             const double2 pw = s_pw[s * (P + 1) + r];
             acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, s_invr[r], d[mt][0]), d[mt][1])));
@@ -510,8 +538,19 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
     acc[mt].y += __shfl_xor_sync(0xffffffffu, acc[mt].y, 1);
     acc[mt].x += __shfl_xor_sync(0xffffffffu, acc[mt].x, 2);
     acc[mt].y += __shfl_xor_sync(0xffffffffu, acc[mt].y, 2);
-    const int r = 8 * mt + (lane >> 2);
+    const int r = 8 * mt + (lane >> 2) + R0;
+    if (!ROW0 && r == 0) continue;  // written with b0 below
     if ((lane & 3) == 0 && r <= p) loc_l[t * (p + 1) + r] = cadd(acc[mt], s_b[r]);
+  }
+  // b_0: the lanes' partials (butterfly: a fixed order), plus row 0 of the first tile when it rides there
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    b0.x += __shfl_xor_sync(0xffffffffu, b0.x, o);
+    b0.y += __shfl_xor_sync(0xffffffffu, b0.y, o);
+  }
+  if (lane == 0) {
+    if (!ROW0) b0 = cadd(b0, acc[0]);
+    loc_l[t * (p + 1)] = cadd(b0, s_b[0]);
   }
 }
 
