@@ -30,19 +30,24 @@ namespace {
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
 // and report the minimal offending index.  (The leaf CSR comes from the sorted keys.)
-// With u != nullptr it also packs (x, y, u) into one 32-byte record per point (input
-// order), so that the gather after the sort reads one DRAM sector per point, not two.
+// With rec != nullptr it also packs (x, y, u, input index) into one 32-byte record per point:
+// in input order (bin_cap = 0: the records the LSD radix passes move), or (bin_cap > 0, the
+// bucket sort) straight into the point's leaf bin, rec[(k bin_cap + slot)], the slot claimed by the
+// same atomic that counts the leaf (one per distinct key of a warp; its lanes take consecutive
+// slots in lane order); a point whose slot is past the bin's capacity is counted but not stored
+// (the build then takes the LSD sort: k_sort_mode).
 __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
                                               int64_t index_base, uint32_t* __restrict__ key, DevStatus* st,
                                               const double* __restrict__ u = nullptr,
                                               double2* __restrict__ rec = nullptr,
-                                              int32_t* __restrict__ hist = nullptr) {
+                                              int32_t* __restrict__ hist = nullptr, int bin_cap = 0) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool valid = i < n;
   uint32_t k = 0xffffffffu;  // lanes past n: a key no point has (they form their own match group)
+  double2 p = make_double2(0.0, 0.0);
   if (valid) {
-    const double2 p = xy[i];
-    if (rec) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
+    p = xy[i];
+    if (rec && !bin_cap) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
       rec[2 * i] = p;
       rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
     }
@@ -54,7 +59,20 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
   }
   if (hist) {  // leaf histogram of every point, one atomic per distinct key of the warp
     const unsigned peers = __match_any_sync(0xffffffffu, k);
-    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[k], __popc(peers));
+    const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    if (!bin_cap) {
+      if (valid && lane == leader) atomicAdd(&hist[k], __popc(peers));
+      return;
+    }
+    int base = 0;
+    if (valid && lane == leader) base = atomicAdd(&hist[k], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int slot = base + __popc(peers & ((1u << lane) - 1u));
+    if (valid && slot < bin_cap) {
+      const int64_t pos = (int64_t)k * bin_cap + slot;
+      rec[2 * pos] = p;
+      rec[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+    }
   }
 }
 
@@ -64,11 +82,12 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
 __global__ void __launch_bounds__(256) k_offsets(const uint32_t* __restrict__ sorted, int64_t n, int64_t K,
                                                  int32_t* __restrict__ off, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
   if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i > n) return;
-  const int64_t prev = i > 0 ? (int64_t)sorted[i - 1] : -1;
-  const int64_t cur = i < n ? (int64_t)sorted[i] : K + 1;
-  for (int64_t k = prev + 1; k <= cur; ++k) off[k] = (int32_t)i;
+  // grid-stride (gated_grid): a gated-off launch costs one wave of blocks, not n / 256
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t prev = i > 0 ? (int64_t)sorted[i - 1] : -1;
+    const int64_t cur = i < n ? (int64_t)sorted[i] : K + 1;
+    for (int64_t k = prev + 1; k <= cur; ++k) off[k] = (int32_t)i;
+  }
 }
 
 // ------------------------------------------------------------------ scan (exclusive, int32)
@@ -400,46 +419,25 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
 }
 
 // ------------------------------------------------------------------ bucket sort (one rank)
-// Stable order by (key, input index) in three streaming passes instead of two LSD radix passes:
-// the keying kernel counts every leaf (k_keys with hist), the exclusive scan of the counts is the
-// leaf CSR itself, k_bucket_scatter drops each point's 32-byte record (x, y, u, input index)
-// into its leaf's range at an atomically claimed slot (one atomic per distinct key of a warp),
-// and k_leaf_order restores input order inside each leaf (a warp ranks each record by counting
-// the smaller input indices of its leaf) while writing the sorted SoA arrays and the
-// permutation.  The scatter is bound by the L2's atomic throughput per leaf counter and the
-// ranking is quadratic in the leaf size, so the bucket sort serves small leaves only: trees
-// with more than LO_MEAN_MAX points per leaf on average, or with a leaf above LO_WARP_MAX
-// points, take the LSD record sort (measured: DESIGN.md §8c).
-constexpr int LO_WARP_MAX = 256;  // points of a leaf ordered by one warp
+// Stable order by (key, input index) in two streaming passes instead of two LSD radix passes:
+// the keying kernel counts every leaf and drops each point's 32-byte record (x, y, u, input
+// index) into its leaf's bin (LO_WARP_MAX records per leaf, slot = the count returned by the
+// atomic: k_keys with bin_cap); the exclusive scan of the counts is the leaf CSR itself; and
+// k_leaf_order restores input order inside each leaf (a warp ranks each record by counting the
+// smaller input indices of its leaf) while writing the sorted SoA arrays and the permutation.
+// The bins take the L2's atomic throughput per leaf counter and (K + 1) LO_WARP_MAX records of
+// scratch, and the ranking is quadratic in the leaf size, so the bucket sort serves small leaves
+// only: trees with more than LO_MEAN_MAX points per leaf on average, or with a leaf above
+// LO_WARP_MAX points, take the LSD record sort (measured: DESIGN.md §8c).
+constexpr int LO_WARP_MAX = 256;  // points of a leaf ordered by one warp = capacity of a leaf's bin
 constexpr int LO_MEAN_MAX = 80;   // mean points per leaf above which the LSD sort is taken directly
-
-__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ key,
-                                                        const double2* __restrict__ xy,
-                                                        const double* __restrict__ u, int64_t n,
-                                                        const int32_t* __restrict__ off, int32_t* __restrict__ cur,
-                                                        double2* __restrict__ rec, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
-  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool v = i < n;
-  const uint32_t k = v ? key[i] : 0xffffffffu;
-  // one atomic per distinct key of the warp; its lanes take consecutive slots in lane order
-  const unsigned peers = __match_any_sync(0xffffffffu, k);
-  const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
-  int base = 0;
-  if (v && lane == leader) base = atomicAdd(&cur[k], __popc(peers));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (!v) return;
-  const int64_t pos = (int64_t)off[k] + base + __popc(peers & ((1u << lane) - 1u));
-  const double2 p = xy[i];
-  rec[2 * pos] = p;
-  rec[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
-}
+constexpr size_t LO_BIN_BYTES_MAX = (size_t)4 << 30;  // bins of one point set (else the LSD sort)
 
 __device__ __forceinline__ int rec_index(const double2* __restrict__ rec, int64_t pos) {
   return (int)__double_as_longlong(rec[2 * pos + 1].y);
 }
 
-// the record at bucket position pos goes to sorted position o: coordinates with a canonical +0
+// the record at bin position pos goes to sorted position o: coordinates with a canonical +0
 // for a -0 (D13, p2p.cu), strength, input index
 __device__ __forceinline__ void lo_write(const double2* __restrict__ rec, int64_t pos, int64_t o,
                                         double2* __restrict__ sxy, double* __restrict__ su,
@@ -451,9 +449,10 @@ __device__ __forceinline__ void lo_write(const double2* __restrict__ rec, int64_
 }
 
 // one warp per bucket (K + 1 buckets: the leaves and the out-of-domain sentinel K): rank of each
-// record = number of records of the bucket with a smaller input index (indices are distinct)
+// record = number of records of the bucket with a smaller input index (indices are distinct);
+// the bucket's records sit in its bin from bb, its sorted range starts at b
 template <int R>
-__device__ __forceinline__ void lo_rank_warp(const int* __restrict__ sidx, int n, int lane, int64_t b,
+__device__ __forceinline__ void lo_rank_warp(const int* __restrict__ sidx, int n, int lane, int64_t bb, int64_t b,
                                              const double2* __restrict__ rec, double2* __restrict__ sxy,
                                              double* __restrict__ su, int32_t* __restrict__ perm) {
   int mine[R], rank[R];
@@ -469,11 +468,11 @@ __device__ __forceinline__ void lo_rank_warp(const int* __restrict__ sidx, int n
   }
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (lane + 32 * r < n) lo_write(rec, b + lane + 32 * r, b + rank[r], sxy, su, perm);
+    if (lane + 32 * r < n) lo_write(rec, bb + lane + 32 * r, b + rank[r], sxy, su, perm);
 }
 
 __global__ void __launch_bounds__(256) k_leaf_order(int64_t nbuckets, const int32_t* __restrict__ off,
-                                                    const double2* __restrict__ rec, double2* __restrict__ sxy,
+                                                    const double2* __restrict__ bins, double2* __restrict__ sxy,
                                                     double* __restrict__ su, int32_t* __restrict__ perm, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
   if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
   __shared__ int sidx[8][LO_WARP_MAX];
@@ -482,18 +481,19 @@ __global__ void __launch_bounds__(256) k_leaf_order(int64_t nbuckets, const int3
   if (k >= nbuckets) return;
   const int64_t b = off[k];
   const int n = off[k + 1] - (int)b;
-  if (n <= 0) return;  // (n <= LO_WARP_MAX: host-checked)
+  if (n <= 0) return;  // (n <= LO_WARP_MAX: the gate)
+  const int64_t bb = k * LO_WARP_MAX;  // the leaf's bin
   int* si = sidx[w];
-  for (int e = lane; e < n; e += 32) si[e] = rec_index(rec, b + e);
+  for (int e = lane; e < n; e += 32) si[e] = rec_index(bins, bb + e);
   __syncwarp();
   if (n <= 32)
-    lo_rank_warp<1>(si, n, lane, b, rec, sxy, su, perm);
+    lo_rank_warp<1>(si, n, lane, bb, b, bins, sxy, su, perm);
   else if (n <= 64)
-    lo_rank_warp<2>(si, n, lane, b, rec, sxy, su, perm);
+    lo_rank_warp<2>(si, n, lane, bb, b, bins, sxy, su, perm);
   else if (n <= 128)
-    lo_rank_warp<4>(si, n, lane, b, rec, sxy, su, perm);
+    lo_rank_warp<4>(si, n, lane, bb, b, bins, sxy, su, perm);
   else
-    lo_rank_warp<8>(si, n, lane, b, rec, sxy, su, perm);
+    lo_rank_warp<8>(si, n, lane, bb, b, bins, sxy, su, perm);
 }
 
 // largest bucket (leaves and the sentinel) of a count array
@@ -509,10 +509,10 @@ __global__ void __launch_bounds__(256) k_max_i32(const int32_t* __restrict__ v, 
 __global__ void k_make_rec(const double2* __restrict__ xy, const double* __restrict__ u, int64_t n,
                            double2* __restrict__ rec, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
   if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  rec[2 * i] = xy[i];
-  rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    rec[2 * i] = xy[i];
+    rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+  }
 }
 
 // ------------------------------------------------------------------ gathers
@@ -821,6 +821,8 @@ __global__ void __launch_bounds__(256) k_offsets_search(const uint32_t* __restri
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+// grid of a grid-stride kernel that may be gated off on the device: at most 8 blocks per SM
+inline unsigned gated_grid(int64_t n, int t) { return (unsigned)std::min<int64_t>((n + t - 1) / t, 148 * 8); }
 
 }  // namespace
 
@@ -913,7 +915,7 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
   if (t->cfg.nranks > 1)
     k_offsets_search<<<blocks_for(t->g.K + 2, 256), 256, 0, s>>>(kin, n, t->g.K, off);
   else
-    k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
+    k_offsets<<<gated_grid(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
@@ -995,7 +997,7 @@ static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2
     rin = rout;
     shift += db;
   }
-  k_offsets<<<blocks_for(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off, gate, 1);
+  k_offsets<<<gated_grid(n + 1, 256), 256, 0, s>>>(kin, n, t->g.K, off, gate, 1);
   t->launches++;
   FMM_CUDA_TRY(cudaGetLastError());
   return FMM_OK;
@@ -1072,10 +1074,12 @@ __global__ void k_sort_mode(const int32_t* __restrict__ mx, int32_t* __restrict_
 }
 
 // one rank (DESIGN.md §7 "Build"), per point set: the LSD record sort when the leaves hold more
-// than LO_MEAN_MAX points on average or the set is small (host decisions); else keys with leaf counts, the leaf CSR
-// from their scan, and both sorts enqueued with every kernel gated by a device mode word -- the
-// bucket sort when no leaf holds more than LO_WARP_MAX points, else the LSD record sort -- so
-// that the build never waits on the device from the host.  FMM_SORT_LSD=1 forces the LSD sort.
+// than LO_MEAN_MAX points on average, the set is small or the leaf bins would not fit (host
+// decisions); else keys with leaf counts and the records dropped into leaf bins, the leaf CSR from
+// the counts' scan, and both sorts enqueued with every kernel gated by a device mode word -- the
+// bucket sort's ordering pass when no leaf holds more than LO_WARP_MAX points, else the LSD record
+// sort -- so that the build never waits on the device from the host.  FMM_SORT_LSD=1 forces the
+// LSD sort.
 static int single_rank_keys_sort(fmm_tree_s* t) {
   cudaStream_t s = t->stream;
   const Geo& G = t->g;
@@ -1087,9 +1091,11 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
   t->m_loc = t->m;
   const char* force = getenv("FMM_SORT_LSD");
   const bool force_lsd = force && force[0] == '1';
+  const size_t bin_bytes = (size_t)(K + 1) * LO_WARP_MAX * 32;
   bool lsd[2];
   // small point sets (<= 2^20: launch-bound builds) skip the gated pair of paths
-  for (int k = 0; k < 2; ++k) lsd[k] = force_lsd || cnt[k] > LO_MEAN_MAX * K || cnt[k] <= (1 << 20);
+  for (int k = 0; k < 2; ++k)
+    lsd[k] = force_lsd || cnt[k] > LO_MEAN_MAX * K || cnt[k] <= (1 << 20) || bin_bytes > LO_BIN_BYTES_MAX;
   // scratch per point set: counts (K + 2) | scan scratch; then two maxima and two mode words
   const size_t sscan = fmm_scan_scratch_bytes(nb);
   const size_t hb = ((size_t)nb * 4 + 255) / 256 * 256;
@@ -1108,14 +1114,16 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
   double2* xy_out[2] = {t->sxy, t->txy};
   double* u_out[2] = {t->su, nullptr};
   int32_t* perm[2] = {t->sperm, t->tperm};
-  double2* rec[2] = {nullptr, nullptr};
+  double2* rec[2] = {nullptr, nullptr};   // records in input order (LSD)
+  double2* bins[2] = {nullptr, nullptr};  // leaf bins (bucket sort)
   for (int k = 0; k < nsets; ++k)
     if (cnt[k] > 0) {
       FMM_CUDA_TRY(cudaMallocAsync((void**)&rec[k], (size_t)cnt[k] * 32, s));
-      // LSD: keys + records in input order (no counts); bucket: keys + counts
-      k_keys<<<blocks_for(cnt[k], 256), 256, 0, s>>>(g, xy[k], cnt[k], k ? t->n : 0, keys[k], t->status,
-                                                      lsd[k] ? u[k] : nullptr, lsd[k] ? rec[k] : nullptr,
-                                                      lsd[k] ? nullptr : hist(k));
+      if (!lsd[k]) FMM_CUDA_TRY(cudaMallocAsync((void**)&bins[k], bin_bytes, s));
+      // LSD: keys + records in input order (no counts); bucket: keys + counts + records into the bins
+      k_keys<<<blocks_for(cnt[k], 256), 256, 0, s>>>(g, xy[k], cnt[k], k ? t->n : 0, keys[k], t->status, u[k],
+                                                      lsd[k] ? rec[k] : bins[k], lsd[k] ? nullptr : hist(k),
+                                                      lsd[k] ? 0 : LO_WARP_MAX);
       t->launches++;
     }
   FMM_CUDA_TRY(cudaGetLastError());
@@ -1137,21 +1145,19 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
     k_sort_mode<<<1, 1, 0, s>>>(mx + k, mode + k);
     t->launches += 2;
     // mode 1: input-order records, then the LSD record sort (its offsets overwrite the same CSR)
-    k_make_rec<<<blocks_for(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k], mode + k, 1);
+    k_make_rec<<<gated_grid(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k], mode + k, 1);
     t->launches++;
     e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k], mode + k);
     if (e) break;
-    // mode 0: the bucket sort; the counts, zeroed, become the per-leaf slot cursors
-    int32_t* cur = hist(k);
-    FMM_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(int32_t) * nb, s));
-    k_bucket_scatter<<<blocks_for(cnt[k], 256), 256, 0, s>>>(keys[k], xy[k], u[k], cnt[k], off[k], cur, rec[k],
-                                                              mode + k, 0);
-    k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], rec[k], xy_out[k], u_out[k], perm[k], mode + k, 0);
-    t->launches += 2;
+    // mode 0: the bucket sort's ordering pass over the bins
+    k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], bins[k], xy_out[k], u_out[k], perm[k], mode + k, 0);
+    t->launches++;
     FMM_CUDA_TRY(cudaGetLastError());
   }
-  for (int k = 0; k < nsets; ++k)
+  for (int k = 0; k < nsets; ++k) {
     if (rec[k]) cudaFreeAsync(rec[k], s);
+    if (bins[k]) cudaFreeAsync(bins[k], s);
+  }
   cudaFreeAsync(buf, s);
   return e;
 }
