@@ -30,16 +30,16 @@ namespace {
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
 // and report the minimal offending index.  (The leaf CSR comes from the sorted keys.)
-// With rec != nullptr it also packs (x, y, u, input index) into one 32-byte record per point:
-// in input order (bin_cap = 0: the records the LSD radix passes move), or (bin_cap > 0, the
-// bucket sort) straight into the point's leaf bin, rec[(k bin_cap + slot)], the slot claimed by the
-// same atomic that counts the leaf (one per distinct key of a warp; its lanes take consecutive
+// With hist != nullptr it also counts every leaf (the multi-rank global histogram), and with
+// bin_cap > 0 (the bucket sort) it packs (x, y, u, input index) into one 32-byte record per point
+// and drops it straight into the point's leaf bin, bins[k bin_cap + slot], the slot claimed by
+// the same atomic that counts the leaf (one per distinct key of a warp; its lanes take consecutive
 // slots in lane order); a point whose slot is past the bin's capacity is counted but not stored
 // (the build then takes the LSD sort: k_sort_mode).
 __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict__ xy, int64_t n,
                                               int64_t index_base, uint32_t* __restrict__ key, DevStatus* st,
                                               const double* __restrict__ u = nullptr,
-                                              double2* __restrict__ rec = nullptr,
+                                              double2* __restrict__ bins = nullptr,
                                               int32_t* __restrict__ hist = nullptr, int bin_cap = 0) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool valid = i < n;
@@ -47,10 +47,6 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
   double2 p = make_double2(0.0, 0.0);
   if (valid) {
     p = xy[i];
-    if (rec && !bin_cap) {  // (x, y, u, input index): the 32-byte record the radix passes move (one rank)
-      rec[2 * i] = p;
-      rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
-    }
     if (!geo_key(g, p.x, p.y, &k)) {
       k = (uint32_t)g.K;
       atomicMin(&st->domain_bad, (unsigned long long)(index_base + i));
@@ -70,8 +66,8 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
     const int slot = base + __popc(peers & ((1u << lane) - 1u));
     if (valid && slot < bin_cap) {
       const int64_t pos = (int64_t)k * bin_cap + slot;
-      rec[2 * pos] = p;
-      rec[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+      bins[2 * pos] = p;
+      bins[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
     }
   }
 }
@@ -293,13 +289,16 @@ __global__ void __launch_bounds__(RS_T) k_radix_count(const uint32_t* __restrict
 // output positions -- leave in coalesced runs instead of one 16-byte store per element.
 // FINAL: the last pass writes the record's fields to their SoA homes (sorted positions with a
 // canonical +0 for a -0 coordinate, D13; strengths when su != NULL; the permutation) and the
-// sorted keys (for the leaf CSR).
+// sorted keys (for the leaf CSR).  FIRST: the first pass forms the records from the caller's
+// arrays (xy_in, u_in or NULL, the position as the input index) instead of reading them.
 constexpr int RR_SEG = 256, RR_TILE = RS_W * RR_SEG;
 constexpr size_t RR_SMEM = sizeof(int) * (RS_W + 2) * (1 << RS_MAXB) + sizeof(uint32_t) * RR_TILE +
                            2 * sizeof(double2) * RR_TILE;
-template <bool FINAL>
+template <bool FINAL, bool FIRST>
 __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __restrict__ keys,
-                                                              const double2* __restrict__ rec, int64_t n, int shift,
+                                                              const double2* __restrict__ rec,
+                                                              const double2* __restrict__ xy_in,
+                                                              const double* __restrict__ u_in, int64_t n, int shift,
                                                               int db, const int32_t* __restrict__ tile_off,
                                                               int ntiles, uint32_t* __restrict__ keys_out,
                                                               double2* __restrict__ rec_out,
@@ -328,8 +327,13 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
   for (int r = 0; r < NR; ++r) {
     const int64_t i = seg0 + 32 * r + lane;
     kr[r] = i < n ? keys[i] : 0u;
-    ra[r] = i < n ? rec[2 * i] : make_double2(0.0, 0.0);
-    rb[r] = i < n ? rec[2 * i + 1] : make_double2(0.0, 0.0);
+    if (FIRST) {
+      ra[r] = i < n ? xy_in[i] : make_double2(0.0, 0.0);
+      rb[r] = make_double2((i < n && u_in) ? u_in[i] : 0.0, __longlong_as_double(i));
+    } else {
+      ra[r] = i < n ? rec[2 * i] : make_double2(0.0, 0.0);
+      rb[r] = i < n ? rec[2 * i + 1] : make_double2(0.0, 0.0);
+    }
   }
   // 1. per-warp digit counts
 #pragma unroll
@@ -503,16 +507,6 @@ __global__ void __launch_bounds__(256) k_max_i32(const int32_t* __restrict__ v, 
     m = max(m, v[i]);
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
-}
-
-// (x, y, u, input index) records in input order (the LSD fallback of the bucket sort)
-__global__ void k_make_rec(const double2* __restrict__ xy, const double* __restrict__ u, int64_t n,
-                           double2* __restrict__ rec, const int32_t* __restrict__ gate = nullptr, int gate_want = 0) {
-  if (gate && *gate != gate_want) return;  // the other sort path runs (single_rank_keys_sort)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    rec[2 * i] = xy[i];
-    rec[2 * i + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
-  }
 }
 
 // ------------------------------------------------------------------ gathers
@@ -926,13 +920,15 @@ static int radix_sort_perm(fmm_tree_s* t, const uint32_t* keys, int64_t n, int32
 // leaves, and the stable compaction of the points it keeps (a second host sync reads their
 // counts).  ckey / cidx (n + m entries each) receive the kept keys and input indices: sources
 // first, then targets (distinct-target trees).
-// stable LSD radix sort of (key, 32-byte record) pairs of one rank's points: the records move
-// with the keys through every pass and the last pass writes the sorted SoA arrays and the
-// permutation; then the leaf CSR off[0..K+1] from the sorted keys
+// stable LSD radix sort of (key, 32-byte record) pairs of one rank's points: the first pass forms
+// the records (x, y, u, input index) from the caller's arrays, they move with the keys through
+// every pass and the last pass writes the sorted SoA arrays and the permutation; then the leaf
+// CSR off[0..K+1] from the sorted keys
 // gate (device int, optional): every kernel of the sort runs only when *gate == 1 (the LSD path of
 // single_rank_keys_sort, decided on the device)
-static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2* rec, int64_t n, double2* xy_out,
-                              double* u_out, int32_t* perm, int32_t* off, const int32_t* gate = nullptr) {
+static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2* xy_in, const double* u_in,
+                              int64_t n, double2* xy_out, double* u_out, int32_t* perm, int32_t* off,
+                              const int32_t* gate = nullptr) {
   cudaStream_t s = t->stream;
   if (n == 0) {
     FMM_CUDA_TRY(cudaMemsetAsync(off, 0, sizeof(int32_t) * (t->g.K + 2), s));
@@ -942,14 +938,11 @@ static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2
   const int passes = (bits + RS_MAXB - 1) / RS_MAXB;
   const int ntiles = (int)((n + RR_TILE - 1) / RR_TILE);
   const int64_t nhist = ((int64_t)1 << ((bits + passes - 1) / passes)) * ntiles;
-  static bool attr_set = false;
-  if (!attr_set) {
-    FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)RR_SMEM));
-    FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)RR_SMEM));
-    attr_set = true;
-  }
+  // per device (a process may drive several GPUs)
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
+  FMM_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter_rec<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
   // scratch: kA kB (n u32), record ping-pong (n x 32 B each: one buffer for two passes, two for
   // more), hist, scan scratch
   const int nrec = passes > 2 ? 2 : (passes > 1 ? 1 : 0);
@@ -975,7 +968,7 @@ static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2
   int32_t* hist = (int32_t*)take((size_t)nhist * 4);
   void* sscr = p;
   const uint32_t* kin = keys;
-  const double2* rin = rec;
+  const double2* rin = nullptr;
   int shift = 0;
   for (int ps = 0; ps < passes; ++ps) {
     const int db = bits / passes + (ps < bits % passes ? 1 : 0);
@@ -985,12 +978,11 @@ static int radix_sort_records(fmm_tree_s* t, const uint32_t* keys, const double2
     k_radix_count<<<ntiles, RS_T, 0, s>>>(kin, n, shift, db, hist, ntiles, RR_TILE, gate, 1);
     int e = device_scan_gated(hist, hist, nh, sscr, fmm_scan_scratch_bytes(nh), s, &t->launches, gate, 1);
     if (e) return e;
-    if (ps == passes - 1)
-      k_radix_scatter_rec<true><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, nullptr,
-                                                              xy_out, u_out, perm, gate, 1);
-    else
-      k_radix_scatter_rec<false><<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, n, shift, db, hist, ntiles, kout, rout,
-                                                               nullptr, nullptr, nullptr, gate, 1);
+    const bool fin = ps == passes - 1;
+    auto kern = fin ? (ps == 0 ? k_radix_scatter_rec<true, true> : k_radix_scatter_rec<true, false>)
+                    : (ps == 0 ? k_radix_scatter_rec<false, true> : k_radix_scatter_rec<false, false>);
+    kern<<<ntiles, RS_T, RR_SMEM, s>>>(kin, rin, xy_in, u_in, n, shift, db, hist, ntiles, kout, fin ? nullptr : rout,
+                                       fin ? xy_out : nullptr, fin ? u_out : nullptr, fin ? perm : nullptr, gate, 1);
     t->launches += 2;
     FMM_CUDA_TRY(cudaGetLastError());
     kin = kout;
@@ -1114,15 +1106,13 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
   double2* xy_out[2] = {t->sxy, t->txy};
   double* u_out[2] = {t->su, nullptr};
   int32_t* perm[2] = {t->sperm, t->tperm};
-  double2* rec[2] = {nullptr, nullptr};   // records in input order (LSD)
   double2* bins[2] = {nullptr, nullptr};  // leaf bins (bucket sort)
   for (int k = 0; k < nsets; ++k)
     if (cnt[k] > 0) {
-      FMM_CUDA_TRY(cudaMallocAsync((void**)&rec[k], (size_t)cnt[k] * 32, s));
       if (!lsd[k]) FMM_CUDA_TRY(cudaMallocAsync((void**)&bins[k], bin_bytes, s));
-      // LSD: keys + records in input order (no counts); bucket: keys + counts + records into the bins
+      // LSD: keys only (its first pass forms the records); bucket: keys + counts + records into the bins
       k_keys<<<blocks_for(cnt[k], 256), 256, 0, s>>>(g, xy[k], cnt[k], k ? t->n : 0, keys[k], t->status, u[k],
-                                                      lsd[k] ? rec[k] : bins[k], lsd[k] ? nullptr : hist(k),
+                                                      lsd[k] ? nullptr : bins[k], lsd[k] ? nullptr : hist(k),
                                                       lsd[k] ? 0 : LO_WARP_MAX);
       t->launches++;
     }
@@ -1136,7 +1126,7 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
       continue;
     }
     if (lsd[k]) {
-      e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k]);
+      e = radix_sort_records(t, keys[k], xy[k], u[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k]);
       continue;
     }
     e = fmm_device_scan_i32(hist(k), off[k], nb, sscr(k), sscan, s, &t->launches);
@@ -1144,20 +1134,16 @@ static int single_rank_keys_sort(fmm_tree_s* t) {
     k_max_i32<<<64, 256, 0, s>>>(hist(k), K + 1, mx + k);
     k_sort_mode<<<1, 1, 0, s>>>(mx + k, mode + k);
     t->launches += 2;
-    // mode 1: input-order records, then the LSD record sort (its offsets overwrite the same CSR)
-    k_make_rec<<<gated_grid(cnt[k], 256), 256, 0, s>>>(xy[k], u[k], cnt[k], rec[k], mode + k, 1);
-    t->launches++;
-    e = radix_sort_records(t, keys[k], rec[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k], mode + k);
+    // mode 1: the LSD record sort (its offsets overwrite the same CSR)
+    e = radix_sort_records(t, keys[k], xy[k], u[k], cnt[k], xy_out[k], u_out[k], perm[k], off[k], mode + k);
     if (e) break;
     // mode 0: the bucket sort's ordering pass over the bins
     k_leaf_order<<<blocks_for(K + 1, 8), 256, 0, s>>>(K + 1, off[k], bins[k], xy_out[k], u_out[k], perm[k], mode + k, 0);
     t->launches++;
     FMM_CUDA_TRY(cudaGetLastError());
   }
-  for (int k = 0; k < nsets; ++k) {
-    if (rec[k]) cudaFreeAsync(rec[k], s);
+  for (int k = 0; k < nsets; ++k)
     if (bins[k]) cudaFreeAsync(bins[k], s);
-  }
   cudaFreeAsync(buf, s);
   return e;
 }
