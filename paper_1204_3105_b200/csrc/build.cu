@@ -27,6 +27,20 @@ DGeo dgeo(const Geo& g) {
 
 namespace {
 
+// One 32-byte record (two double2, 32-byte aligned) moved by a single 256-bit global access
+// (sm_100: LDG / STG .ENL2.256), so that a scattered record costs one L2 transaction per lane, not two.
+__device__ __forceinline__ void st_rec(double2* __restrict__ rec, int64_t pos, double2 a, double2 b) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(rec + 2 * pos), "l"(__double_as_longlong(a.x)),
+               "l"(__double_as_longlong(a.y)), "l"(__double_as_longlong(b.x)), "l"(__double_as_longlong(b.y))
+               : "memory");
+}
+__device__ __forceinline__ void ld_rec(const double2* __restrict__ rec, int64_t pos, double2* a, double2* b) {
+  long long x, y, z, w;
+  asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];" : "=l"(x), "=l"(y), "=l"(z), "=l"(w) : "l"(rec + 2 * pos));
+  *a = make_double2(__longlong_as_double(x), __longlong_as_double(y));
+  *b = make_double2(__longlong_as_double(z), __longlong_as_double(w));
+}
+
 // ------------------------------------------------------------------ keying
 // key per point; out-of-domain points get the sentinel key K (sorted past every leaf)
 // and report the minimal offending index.  (The leaf CSR comes from the sorted keys.)
@@ -65,9 +79,7 @@ __global__ void __launch_bounds__(256) k_keys(DGeo g, const double2* __restrict_
     base = __shfl_sync(0xffffffffu, base, leader);
     const int slot = base + __popc(peers & ((1u << lane) - 1u));
     if (valid && slot < bin_cap) {
-      const int64_t pos = (int64_t)k * bin_cap + slot;
-      bins[2 * pos] = p;
-      bins[2 * pos + 1] = make_double2(u ? u[i] : 0.0, __longlong_as_double(i));
+      st_rec(bins, (int64_t)k * bin_cap + slot, p, make_double2(u ? u[i] : 0.0, __longlong_as_double(i)));
     }
   }
 }
@@ -331,8 +343,8 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
       ra[r] = i < n ? xy_in[i] : make_double2(0.0, 0.0);
       rb[r] = make_double2((i < n && u_in) ? u_in[i] : 0.0, __longlong_as_double(i));
     } else {
-      ra[r] = i < n ? rec[2 * i] : make_double2(0.0, 0.0);
-      rb[r] = i < n ? rec[2 * i + 1] : make_double2(0.0, 0.0);
+      ra[r] = rb[r] = make_double2(0.0, 0.0);
+      if (i < n) ld_rec(rec, i, &ra[r], &rb[r]);
     }
   }
   // 1. per-warp digit counts
@@ -416,8 +428,7 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter_rec(const uint32_t* __re
       if (su) su[g] = b.x;
       perm[g] = (int32_t)__double_as_longlong(b.y);
     } else {
-      rec_out[2 * g] = a;
-      rec_out[2 * g + 1] = b;
+      st_rec(rec_out, g, a, b);
     }
   }
 }
@@ -446,7 +457,8 @@ __device__ __forceinline__ int rec_index(const double2* __restrict__ rec, int64_
 __device__ __forceinline__ void lo_write(const double2* __restrict__ rec, int64_t pos, int64_t o,
                                         double2* __restrict__ sxy, double* __restrict__ su,
                                         int32_t* __restrict__ perm) {
-  const double2 a = rec[2 * pos], b = rec[2 * pos + 1];
+  double2 a, b;
+  ld_rec(rec, pos, &a, &b);
   sxy[o] = make_double2(__dadd_rn(a.x, 0.0), __dadd_rn(a.y, 0.0));
   if (su) su[o] = b.x;
   perm[o] = (int)__double_as_longlong(b.y);
