@@ -107,8 +107,10 @@ def test_host_inputs_match_device_inputs():
     assert np.array_equal(a, out)
 
 
-@pytest.mark.parametrize("p", [1, 5, 31])
+@pytest.mark.parametrize("p", [1, 5, 10, 14, 27, 31])
 def test_expansion_orders(p):
+    """every template order of the downward kernel (P = 8, 12, 16, 28, 32 here; 16, 20, 24 in the
+    configs): row 0 of the M2L contraction is formed outside the DMMA tiles when P % 8 == 0"""
     w = SMALL_CASES["C2"].scaled(3000)
     d = data(w)
     phi = gpu_tree(w, d, p=p).evaluate().cpu().numpy()
