@@ -365,3 +365,35 @@ def test_p2p_pairing_variants(name, pairs, monkeypatch):
     g.check()
     assert normwise(phi, oracle_tree(w, d).evaluate()) <= TOL
     assert np.array_equal(phi, g.evaluate().cpu().numpy()) or name == "C5s"  # C5s: heavy blocks (atomics)
+
+
+@pytest.mark.parametrize("case,depth", [("C4qs", 12), ("C4ts", 12), ("C4ss", 9)])
+def test_maximum_depth(case, depth):
+    """The deepest trees fmm_build_tree accepts (include/fmm_b200.h: depth 12 for the quadtree and
+    the triangle-quadtree, 9 for the septree: 16.8M / 40.4M leaves, nearly all of them empty) on
+    20,000 points: keys, sort order and leaf CSR bit for bit against the oracle (P:76, P:79,
+    P:207-250), potentials within the D15 gate of the oracle FMM at the same depth.
+    The septree's points are drawn in the depth-6 island and pulled towards its centre, since the
+    island's boundary changes with the depth."""
+    import oracle
+
+    from paper_1204_3105_b200 import X
+
+    w = SMALL_CASES[case].scaled(20000, name=f"max-{case}")
+    d = dict(data(w))
+    if w.tiling == SMALL_CASES["C4ss"].tiling:
+        c = np.array([w.root_x, w.root_y])
+        d["src_xy"] = c + 0.6 * (d["src_xy"] - c)
+    g = gpu_tree(w, d, p=4, depth=depth)
+    cfg = oracle.config(w.tiling, depth, 4, w.root_x, w.root_y, w.root_size, True)
+    sk = oracle.keys(cfg, d["src_xy"])
+    K = (7 if w.tiling == SMALL_CASES["C4ss"].tiling else 4) ** depth
+    assert sk.max() < K
+    assert np.array_equal(g.export(X.SRC_KEYS), sk)
+    sp = np.argsort(sk, kind="stable").astype(np.int32)
+    assert np.array_equal(g.export(X.SRC_PERM), sp)
+    so = np.searchsorted(sk[sp], np.arange(K + 1)).astype(np.int64)
+    assert np.array_equal(g.export(X.SRC_OFFSETS), so)
+    phi = g.evaluate().cpu().numpy()
+    g.check()
+    assert normwise(phi, oracle_tree(w, d, p=4, depth=depth).evaluate()) <= TOL
