@@ -108,3 +108,36 @@ def test_fullsize_within_paper_bound_of_direct_sum(cache, name):
     direct = oracle.direct(d["src_xy"], d["u"], d["tgt_xy"], w.self_mode, ids)
     bound = o.bound(ids)
     assert np.all(np.abs(phi[ids].real - direct.real) <= bound)
+
+
+def test_maximum_point_count():
+    """The largest point set fmm_build_tree accepts (include/fmm_b200.h: 2^27 points per set, the
+    capacity of the device scans: here the radix sort's digit histogram is exactly 2^26 entries)
+    on the quadtree of depth 11 (32 points per leaf): keys, sort order and leaf CSR of every point
+    bit for bit against the oracle's keys in stable order; the real part of the
+    potentials of 8 seeded targets (D13 / D14: the far field's Arg may sit on another branch than
+    the direct sum's) against the oracle's direct sum over all 2^27 sources -- a lost, duplicated
+    or misplaced source moves a potential by ~1e-4 of max |Phi|, the truncation at p = 24 by
+    ~1e-11 (profiles/r01/sweep_next1.json), the gate is 1e-7."""
+    import oracle
+
+    from paper_1204_3105_b200 import X
+
+    n, depth = 1 << 27, 11
+    w = fi.get("C4q").scaled(n, name="max-n")
+    d = fi.generate(w)
+    g = gpu_tree(w, d, depth=depth)
+    phi = g.evaluate()
+    g.check()
+    cfg = oracle.config(w.tiling, depth, w.p, w.root_x, w.root_y, w.root_size, True)
+    sk = oracle.keys(cfg, d["src_xy"])
+    assert np.array_equal(g.export(X.SRC_KEYS), sk)
+    sp = np.argsort(sk, kind="stable").astype(np.int32)
+    assert np.array_equal(g.export(X.SRC_PERM), sp)
+    so = np.searchsorted(sk[sp], np.arange(4 ** depth + 1)).astype(np.int64)
+    del sp
+    assert np.array_equal(g.export(X.SRC_OFFSETS), so)
+    ids = np.sort(np.random.default_rng(11).choice(n, size=8, replace=False))
+    got = phi[ids.tolist()].cpu().numpy()
+    direct = oracle.direct(d["src_xy"], d["u"], None, True, ids)
+    assert np.abs(got.real - direct.real).max() <= 1e-7 * np.abs(direct.real).max()
