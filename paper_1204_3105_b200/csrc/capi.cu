@@ -210,6 +210,7 @@ void carve(fmm_tree_s* t, Arena& a) {
   t->mp = a.take<double2>(G.total_cells * (G.p + 1));
   t->loc = a.take<double2>(G.total_cells * (G.p + 1));
   t->binom = a.take<double>((size_t)BS * BS);
+  t->afr = a.take<double>(FMM_AFR_MAX);
   t->status = a.take<DevStatus>(1);
 }
 
@@ -444,11 +445,18 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   static std::once_flag hconst_once;
   std::call_once(hconst_once, [] {
     const size_t nb = (size_t)BS * BS;
-    hconst_err = cudaHostAlloc((void**)&hconst, (nb + P2P_TAB_DOUBLES) * sizeof(double), cudaHostAllocPortable);
+    hconst_err = cudaHostAlloc((void**)&hconst, (nb + P2P_TAB_DOUBLES + 7 * FMM_AFR_MAX) * sizeof(double),
+                               cudaHostAllocPortable);
     if (hconst_err != cudaSuccess) return;
     std::vector<double> hb = host_binom();
     memcpy(hconst, hb.data(), nb * sizeof(double));
     fmm_host_p2p_tables(hconst + nb);
+    // the downward kernel's A fragments for every template order 8, 12, ..., 32
+    for (int i = 0; i < 7; ++i) {
+      double* dst = hconst + nb + P2P_TAB_DOUBLES + (size_t)i * FMM_AFR_MAX;
+      memset(dst, 0, sizeof(double) * FMM_AFR_MAX);
+      fmm_down_afr_fill(8 + 4 * i, hb.data(), dst);
+    }
   });
   ce = hconst_err;
   if (ce == cudaSuccess)
@@ -456,6 +464,10 @@ int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* sr
   if (ce == cudaSuccess)
     ce = cudaMemcpyAsync(t->p2p_tab, hconst + (size_t)BS * BS, P2P_TAB_DOUBLES * sizeof(double),
                          cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(t->afr,
+                         hconst + (size_t)BS * BS + P2P_TAB_DOUBLES + (size_t)((fmm_down_order(g.p) - 8) / 4) * FMM_AFR_MAX,
+                         FMM_AFR_MAX * sizeof(double), cudaMemcpyHostToDevice, s);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(t->status, 0xff, sizeof(DevStatus), s);
   if (ce != cudaSuccess) {
     fmm_set_error_message(cudaGetErrorString(ce));

@@ -88,6 +88,7 @@ struct fmm_tree_s {
   double2* mp;     // [total_cells][p+1]
   double2* loc;    // [total_cells][p+1]
   double* binom;   // [(2P+1)][(2P+1)] binomial table
+  double* afr;     // [FMM_AFR_MAX] the downward kernel's DMMA A fragments + 1/r table (fmm_down_afr_fill)
   // status
   DevStatus* status;
   // multi-rank leaf range and the multipole exchange
@@ -137,6 +138,11 @@ int64_t fmm_scan_max_entries();  // largest input of fmm_device_scan_i32 (8192^2
 // counts and the radix digit histograms (1024 per 2048-point tile) must fit one scan
 constexpr int64_t FMM_MAX_POINTS = (int64_t)1 << 27;
 // passes.cu
+// the downward kernel's per-order constants: the DMMA A fragments of the signed binomial matrix and
+// the 1/r table, in the kernel's shared-memory layout, for template order P(p); binom = host table
+constexpr int FMM_AFR_MAX = 4 * 8 * 32 + 8 * 4 + 8;
+int fmm_down_order(int p);  // template order of p: 8, 12, ..., 32
+int fmm_down_afr_fill(int P, const double* binom, double* out);  // returns the doubles written
 int fmm_stage_upward(fmm_tree_s* t);
 int fmm_stage_downward(fmm_tree_s* t);
 int fmm_stage_p2p_pairs(fmm_tree_s* t);

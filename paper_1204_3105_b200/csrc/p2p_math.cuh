@@ -101,6 +101,12 @@ __device__ __forceinline__ double2 p2p_lds2(uint32_t addr) {
   return v;
 }
 
+// entry i of a table of double2: a 32-bit shared-space address (the pair kernel, direct sum and
+// debug hook keep their tables in shared memory) or a global pointer (the M2L's few Log terms per
+// cell read the tables through L1 instead of staging 16 KB of them per block)
+__device__ __forceinline__ double2 p2p_tab_entry(uint32_t smem_addr, uint32_t i) { return p2p_lds2(smem_addr + 16 * i); }
+__device__ __forceinline__ double2 p2p_tab_entry(const double2* __restrict__ gtab, uint32_t i) { return __ldg(gtab + i); }
+
 // shared-space address of a table, laundered through an opaque move so that the compiler keeps
 // it in a register instead of re-deriving the shared window address at every use
 __device__ __forceinline__ uint32_t p2p_smem_addr(const void* p) {
@@ -112,15 +118,15 @@ __device__ __forceinline__ uint32_t p2p_smem_addr(const void* p) {
 // log(r2) = kd * ln 2 + lz for a normal r2 >= 1e-60 (N-entry log table in shared memory).
 // The N intervals of z are centred so that z = 1 is the centre of its interval
 // (c = 1, 1/c = 1, log c = 0): log(1) = 0 exactly, which the self-pair exclusion relies on.
-template <int N = P2P_LOG_N>
-__device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double* kd, double* lz) {
+template <int N = P2P_LOG_N, class TAB = uint32_t>
+__device__ __forceinline__ void p2p_log_split(double r2, TAB logtab, double* kd, double* lz) {
   using T = P2PLogTab<N>;
   int hi = __double2hiint(r2), lo = __double2loint(r2);
   int tmp = hi - T::OFF_HI;
   int i = (tmp >> (T::SHIFT - 32)) & (N - 1);
   int k = tmp >> 20;  // arithmetic shift
   double z = __hiloint2double(hi - (tmp & 0xfff00000), lo);
-  const double2 cl = p2p_lds2(logtab + 16 * i);  // (1/c_i, log c_i)
+  const double2 cl = p2p_tab_entry(logtab, (uint32_t)i);  // (1/c_i, log c_i)
   double r = fma(z, cl.x, -1.0);
   double r_2 = r * r;
   double q;
@@ -138,10 +144,10 @@ __device__ __forceinline__ void p2p_log_split(double r2, uint32_t logtab, double
   *kd = (double)k;
 }
 
-template <int N = P2P_LOG_N>
-__device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
+template <int N = P2P_LOG_N, class TAB = uint32_t>
+__device__ __forceinline__ double p2p_log(double r2, TAB logtab) {
   double kd, lz;
-  p2p_log_split<N>(r2, logtab, &kd, &lz);
+  p2p_log_split<N, TAB>(r2, logtab, &kd, &lz);
   return fma(kd, P2P_C[10], lz) + kd * P2P_C[11];
 }
 
@@ -152,8 +158,8 @@ __device__ __forceinline__ double p2p_log(double r2, uint32_t logtab) {
 // kernel, direct sum, debug hook): |q| <= 1/512, atan q to q^5 (truncation < 2^-56.8 |q|);
 // else the compact 8 x 65 copy with knots k / 64 (M2L), where k must be <= 64 (|z| normal):
 // |q| <= 1/128, atan q to q^7
-template <bool SPARSE>
-__device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab) {
+template <bool SPARSE, class TAB = uint32_t>
+__device__ __forceinline__ double p2p_atan2(double dy, double dx, TAB atab) {
   // Rotation by the reference direction theta of (octant, k): with (P, Q) = (dy, dx), or
   // (-dx, dy) when |dy| > |dx|, and the table's signed slope tau (+-k/64; its sign folds the
   // octant's orientation), Arg z = theta + atan(q), q = (P - tau Q) / (Q + tau P) -- no sign
@@ -185,7 +191,7 @@ __device__ __forceinline__ double p2p_atan2(double dy, double dx, uint32_t atab)
     const int oct = (int)swap | (((unsigned)hx >> 30) & 2) | (((unsigned)hy >> 29) & 4);
     idx = oct * (P2P_ATAN_K + 1) + (k & 0x7f);
   }
-  const double2 Tt = p2p_lds2(atab + 16 * idx);  // (theta[oct][k], tau[oct][k])
+  const double2 Tt = p2p_tab_entry(atab, idx);  // (theta[oct][k], tau[oct][k])
   const double a = fma(-Tt.y, Q, P);
   const double b = fma(Tt.y, P, Q);
   // q = a / b: q0 = a r0 beside the residual e = 1 - b r0, then q0 (1 + e + e^2)

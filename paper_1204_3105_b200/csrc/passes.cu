@@ -345,18 +345,19 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-// shared memory of one k_down_mma block (dynamic): P2P log / atan tables (b_0's Log), the
-// binomial A fragments, then per warp: powers, a~, L2L part, Q, source ids
+// shared memory of one k_down_mma block (dynamic): the binomial A fragments and the 1/r table
+// (copied from the tree's precomputed fmm_down_afr_fill image), then per warp: powers, a~, L2L
+// part, Q, source ids.  b_0's Log reads the P2P log / atan tables from global memory (L1).
 template <int P>
 struct DownSmem {
   static constexpr bool ROW0 = P % 8 == 0;  // row l = 0 formed outside the DMMA tiles
   static constexpr int R0 = ROW0 ? 1 : 0;   // first row of the tiles
   static constexpr int NB = 8, MT = ROW0 ? P / 8 : (P + 8) / 8, KT = P / 4;  // rows R0 .. R0 + 8 MT - 1
-  static constexpr size_t tab = sizeof(double2) * (P2P_LOGC_N + 8 * (P2P_ATAN_K + 1));
-  static constexpr size_t afr = sizeof(double) * (MT * KT * 32 + 8 * MT + 8);  // + 1/r table, r = 0..8 MT
+  static constexpr int afr_n = MT * KT * 32 + 8 * MT + 8;  // A fragments + 1/r table, r = 0..8 MT (+ padding)
+  static constexpr size_t afr = sizeof(double) * afr_n;
   static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + 32) + sizeof(double) * NB +
                                  sizeof(int) * FMM_CAND_MAX;
-  static constexpr size_t bytes = tab + afr + 4 * warp;
+  static constexpr size_t bytes = afr + 4 * warp;
 };
 
 #ifndef DOWN_MINB
@@ -374,34 +375,28 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
                                                      const unsigned long long* __restrict__ e4mask,
                                                      const double2* __restrict__ mp_l, int p,
                                                      const double* __restrict__ binom, const double* __restrict__ tabs,
-                                                     double2* __restrict__ loc_l) {
+                                                     const double* __restrict__ afr, double2* __restrict__ loc_l) {
   using S = DownSmem<P>;
   constexpr int NB = S::NB, MT = S::MT, KT = S::KT, R0 = S::R0;
   constexpr bool ROW0 = S::ROW0;
   extern __shared__ double2 dsm[];
-  double2* s_log = dsm;
-  double2* s_atan = s_log + P2P_LOGC_N;
-  double* s_afr = (double*)((char*)dsm + S::tab);
+  double* s_afr = (double*)dsm;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  char* wb = (char*)dsm + S::tab + S::afr + w * S::warp;
+  char* wb = (char*)dsm + S::afr + w * S::warp;
   double2* s_pw = (double2*)wb;          // [NB][P+1] w_s^k
   double2* s_at = s_pw + NB * (P + 1);   // [NB][P]   a~_{s,k}, k = 1..P
   double2* s_b = s_at + NB * P;          // [32]      L2L part
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
-  p2p_load_tables_compact(tabs, s_log, s_atan);  // ends with __syncthreads
-  // A fragments: Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in), row r = 8 mt + ln/4 + R0,
-  // column k = 4 kt + ln%4 + 1
-  for (int i = threadIdx.x; i < MT * KT * 32; i += blockDim.x) {
-    const int ln = i & 31, kt = (i >> 5) % KT, mt = (i >> 5) / KT;
-    const int r = 8 * mt + (ln >> 2) + R0, k = 4 * kt + (ln & 3) + 1;
-    const double c = (r <= p && k <= p) ? binom[(r + k - 1) * BS + (k - 1)] : 0.0;
-    s_afr[i] = (k & 1) ? -c : c;
-  }
-  double* s_invr = s_afr + MT * KT * 32;  // [8 MT + 1] 1/r (0 for r = 0)
-  for (int i = threadIdx.x; i <= 8 * MT; i += blockDim.x) s_invr[i] = i > 0 ? 1.0 / i : 0.0;
+  // A fragments Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in; row r = 8 mt + ln/4 + R0,
+  // column k = 4 kt + ln%4 + 1, at (mt KT + kt) 32 + ln) and the 1/r table behind them: one
+  // coalesced copy of the image fmm_down_afr_fill built for this order
+  for (int i = threadIdx.x; i < S::afr_n; i += blockDim.x) s_afr[i] = afr[i];
+  const double* s_invr = s_afr + MT * KT * 32;  // [8 MT + 1] 1/r (0 for r = 0)
   __syncthreads();
-  const uint32_t a_log = p2p_smem_addr(s_log), a_atan = p2p_smem_addr(s_atan);
+  // b_0's Log: the compact log / atan tables of the P2P math, read from global memory
+  const double2* a_log = (const double2*)tabs + P2P_TAB_LOGC / 2;
+  const double2* a_atan = (const double2*)tabs + P2P_TAB_ATANC / 2;
   const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // cells [cell0, ncells)
   if (t >= ncells) return;
   const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
@@ -447,8 +442,8 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
     const double2 cs = cen_l[src];
     const double Q = mp_l[(int64_t)src * (p + 1)].x;
     const double dx = ct.x - cs.x, dy = __dadd_rn(ct.y - cs.y, 0.0);
-    b0.x = fma(Q, 0.5 * p2p_log<P2P_LOGC_N>(fma(dx, dx, dy * dy), a_log), b0.x);
-    b0.y = fma(Q, p2p_atan2<false>(dy, dx, a_atan), b0.y);
+    b0.x = fma(Q, 0.5 * p2p_log<P2P_LOGC_N, const double2*>(fma(dx, dx, dy * dy), a_log), b0.x);
+    b0.y = fma(Q, p2p_atan2<false, const double2*>(dy, dx, a_atan), b0.y);
   }
   for (int b0s = 0; b0s < nsrc; b0s += NB) {
     const int nb = min(NB, nsrc - b0s);
@@ -554,6 +549,36 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   }
 }
 
+int fmm_down_order(int p) { return p <= 8 ? 8 : (p + 3) / 4 * 4; }
+
+template <int P>
+static int afr_fill(const double* binom, double* out) {
+  using S = DownSmem<P>;
+  for (int i = 0; i < S::MT * S::KT * 32; ++i) {
+    const int ln = i & 31, kt = (i >> 5) % S::KT, mt = (i >> 5) / S::KT;
+    const int r = 8 * mt + (ln >> 2) + S::R0, k = 4 * kt + (ln & 3) + 1;
+    // rows r > p are never written and columns k > p meet zero coefficients, so the image
+    // depends on the order P only
+    const double c = binom[(size_t)(r + k - 1) * BS + (k - 1)];
+    out[i] = (k & 1) ? -c : c;
+  }
+  double* invr = out + S::MT * S::KT * 32;
+  for (int i = 0; i <= 8 * S::MT; ++i) invr[i] = i > 0 ? 1.0 / i : 0.0;
+  return S::afr_n;
+}
+
+int fmm_down_afr_fill(int P, const double* binom, double* out) {
+  switch (P) {
+    case 8: return afr_fill<8>(binom, out);
+    case 12: return afr_fill<12>(binom, out);
+    case 16: return afr_fill<16>(binom, out);
+    case 20: return afr_fill<20>(binom, out);
+    case 24: return afr_fill<24>(binom, out);
+    case 28: return afr_fill<28>(binom, out);
+    default: return afr_fill<32>(binom, out);
+  }
+}
+
 template <int P>
 static void launch_down(fmm_tree_s* t, int l) {
   const Geo& G = t->g;
@@ -569,7 +594,7 @@ static void launch_down(fmm_tree_s* t, int l) {
     k_down_mma<P><<<(unsigned)((nc * 32 + 127) / 128), 128, DownSmem<P>::bytes, t->stream>>>(
         l, G.B, c0, c1, G.ncells[G.L - l] /* B^(L-l) */, t->toff, t->leaf_lo, t->leaf_hi, t->centre + G.lvl_off[l],
         t->centre + G.lvl_off[l - 1], t->loc + G.lvl_off[l - 1] * (p + 1), t->cand + G.lvl_off[l - 1] * FMM_CAND_MAX,
-        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->p2p_tab,
+        t->e4mask + G.lvl_off[l], t->mp + G.lvl_off[l] * (p + 1), p, t->binom, t->p2p_tab, t->afr,
         t->loc + G.lvl_off[l] * (p + 1));
     return;
   }
