@@ -76,16 +76,6 @@ __device__ __forceinline__ void p2p_load_tables(const double* __restrict__ tabs,
   __syncthreads();
 }
 
-// compact copies for the M2L: s_log[P2P_LOGC_N] (p2p_log<P2P_LOGC_N>) and, for p2p_atan2<false>,
-// s_atan[8 * (P2P_ATAN_K + 1)], entry oct * 65 + k
-__device__ __forceinline__ void p2p_load_tables_compact(const double* __restrict__ tabs, double2* s_log,
-                                                        double2* s_atan) {
-  const double2* t2 = (const double2*)tabs;
-  for (int i = threadIdx.x; i < P2P_LOGC_N; i += blockDim.x) s_log[i] = t2[P2P_TAB_LOGC / 2 + i];
-  for (int i = threadIdx.x; i < 8 * (P2P_ATAN_K + 1); i += blockDim.x) s_atan[i] = t2[P2P_TAB_ATANC / 2 + i];
-  __syncthreads();
-}
-
 __device__ __forceinline__ double p2p_rcp(double b) {
   double r0;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(b));

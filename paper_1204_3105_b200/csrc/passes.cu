@@ -361,8 +361,10 @@ struct DownSmem {
 };
 
 #ifndef DOWN_MINB
-#define DOWN_MINB(P) ((P) >= 24 ? 4 : 5)  // resident blocks per SM (register budget 128 / 102): p = 20 at 5 blocks (96
-                                           // registers, no spill) is 6 % faster than at 4; p = 24 at 5 spills (+22 %), p = 16 at 6 spills (+4 %)
+// resident blocks per SM (register budget 128 / 102 / 85): measured with the 33 KB blocks of the
+// precomputed fragment image -- p = 24 at 5 blocks (96 registers, 12 bytes of spill) is 3-4 %
+// faster than at 4, p <= 20 at 6 blocks (80 registers) 2.5-3.5 % faster than at 5; p >= 28 spills at 5
+#define DOWN_MINB(P) ((P) >= 28 ? 4 : ((P) >= 24 ? 5 : 6))
 #endif
 template <int P>
 __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, int64_t cell0, int64_t ncells,
