@@ -390,6 +390,22 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   double2* s_b = s_at + NB * P;          // [32]      L2L part
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
+  // the cell's own loads (everything that depends on t alone: target counts, E4 mask, centres, the
+  // parent's candidates and local expansion), issued before the block's fragment copy so that one
+  // memory round trip covers them all; a warp past the last cell reads the last cell's
+  const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // cells [cell0, ncells)
+  const int64_t tc = min(t, ncells - 1), par = tc / B;
+  const int64_t tlo = max(tc * span_l, leaf_lo), thi = min((tc + 1) * span_l, leaf_hi);
+  const int n_lo = toff[tlo], n_hi = toff[thi];
+  const unsigned long long mask = e4mask[tc];
+  const double2 ct = cen_l[tc];
+  const int32_t* cd = cand + par * FMM_CAND_MAX;
+  const int cd0 = cd[lane], cd1 = cd[lane + 32];
+  double2 cpp = make_double2(0.0, 0.0), lpar = make_double2(0.0, 0.0);
+  if (l >= 2) {
+    cpp = cen_par[par];
+    if (lane <= p) lpar = loc_par[par * (p + 1) + lane];
+  }
   // A fragments Cb[r][k] = (-1)^k C(r+k-1, k-1) (the sign of a~ folded in; row r = 8 mt + ln/4 + R0,
   // column k = 4 kt + ln%4 + 1, at (mt KT + kt) 32 + ln) and the 1/r table behind them: one
   // coalesced copy of the image fmm_down_afr_fill built for this order
@@ -399,28 +415,21 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
   // b_0's Log: the compact log / atan tables of the P2P math, read from global memory
   const double2* a_log = (const double2*)tabs + P2P_TAB_LOGC / 2;
   const double2* a_atan = (const double2*)tabs + P2P_TAB_ATANC / 2;
-  const int64_t t = cell0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // cells [cell0, ncells)
   if (t >= ncells) return;
-  const int64_t tlo = max(t * span_l, leaf_lo), thi = min((t + 1) * span_l, leaf_hi);
-  if (thi <= tlo || toff[thi] == toff[tlo]) return;  // no targets of this rank below t
-  const double2 ct = cen_l[t];
-  const int64_t par = t / B;
+  if (thi <= tlo || n_hi == n_lo) return;  // no targets of this rank below t
   // ---- E4(t) source ids, ascending: lane i places candidates i and i + 32 by prefix popcount
-  const unsigned long long mask = e4mask[t];
-  const int32_t* cd = cand + par * FMM_CAND_MAX;
   {
     const unsigned lo = (unsigned)mask, hi = (unsigned)(mask >> 32), below = (1u << lane) - 1u;
-    if ((lo >> lane) & 1u) s_src[__popc(lo & below)] = cd[lane];
-    if ((hi >> lane) & 1u) s_src[__popc(lo) + __popc(hi & below)] = cd[lane + 32];
+    if ((lo >> lane) & 1u) s_src[__popc(lo & below)] = cd0;
+    if ((hi >> lane) & 1u) s_src[__popc(lo) + __popc(hi & below)] = cd1;
   }
   const int nsrc = __popcll(mask);
   // ---- L2L (lane = coefficient): Horner in w = c_t - c_par over k = p..l
   {
     double2 acc = make_double2(0.0, 0.0);
     if (l >= 2) {
-      const double2 cpp = cen_par[par];
       const double2 wv = make_double2(ct.x - cpp.x, ct.y - cpp.y);
-      s_b[lane] = lane <= p ? loc_par[par * (p + 1) + lane] : make_double2(0.0, 0.0);
+      s_b[lane] = lpar;
       __syncwarp();
 #pragma unroll
       for (int k = P; k >= 0; --k) {  // unrolled: the binomial loads leave the Horner chain
