@@ -98,10 +98,11 @@ __global__ void __launch_bounds__(128) k_p2m(const double2* __restrict__ sxy, co
 }
 
 // ------------------------------------------------------------------ M2M (one warp per parent, lane = coefficient)
-// All B children's multipoles (and the binomial rows) are staged in shared memory first, with
-// one load latency for all of them, and lane k then runs the B children's Horner chains in
-// step (B independent chains: the latency of one is hidden by the others); the children are
-// added in ascending order as before.
+// All B children's multipoles are staged in shared memory first, with one load latency for all
+// of them, and lane k then runs the B children's Horner chains in step (B independent chains:
+// the latency of one is hidden by the others); the children are added in ascending order as
+// before.  The binomials C(k - 1, j - 1) of lane k's row are read from the global table (L1)
+// in the chain: staging a 32 x 32 table per block of four parents cost more than it saved.
 template <int B>
 __global__ void __launch_bounds__(128) k_m2m(int64_t par0, int64_t nparents, int64_t span_l,
                                              const int32_t* __restrict__ soff,
@@ -110,13 +111,7 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t par0, int64_t nparents, int
                                              double2* __restrict__ mp_par) {
   __shared__ double2 s_a[4][B][32];
   __shared__ double2 s_z[4][B];   // c_child - c_parent of the staged children
-  __shared__ double s_c[32][33];  // s_c[k][j] = C(k - 1, j - 1)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-    const int k = i >> 5, j = i & 31;
-    s_c[k][j] = (k >= 1 && j >= 1 && j <= k) ? binom[(k - 1) * BS + (j - 1)] : 0.0;
-  }
-  __syncthreads();
   const int64_t P = par0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // parents [par0, nparents)
   if (P >= nparents) return;
   const double2 cp = cen_par[P];
@@ -149,8 +144,9 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t par0, int64_t nparents, int
         h[q] = make_double2(v ? -s_a[w][q0 + q][0].x / k : 0.0, 0.0);
         z0[q] = v ? s_z[w][q0 + q] : make_double2(0.0, 0.0);
       }
+      const double* crow = binom + (k - 1) * BS - 1;  // crow[j] = C(k - 1, j - 1)
       for (int j = 1; j <= k; ++j) {
-        const double cj = s_c[k][j];
+        const double cj = __ldg(crow + j);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const double2 a = q0 + q < nc ? s_a[w][q0 + q][j] : make_double2(0.0, 0.0);
