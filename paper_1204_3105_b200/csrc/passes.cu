@@ -21,6 +21,10 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+// c + a b in four fused multiply-adds (cadd(c, cmul(a, b)) takes two multiplies, two FMAs and two adds)
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
 __device__ __forceinline__ double2 cinv(double2 z) {
   double d = 1.0 / (z.x * z.x + z.y * z.y);
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
       for (int k = P; k >= 0; --k) {  // unrolled: the binomial loads leave the Horner chain
         if (k > p) continue;
         const double2 bk = s_b[k];
-        if (k >= lane && lane <= p) acc = cadd(cmul(acc, wv), cscale(binom[k * BS + lane], bk));
+        if (k >= lane && lane <= p) acc = cfma(acc, wv, cscale(binom[k * BS + lane], bk));
       }
       __syncwarp();
     }
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
             acc[mt].y += d[mt][1];
           } else {
             const double2 pw = s_pw[s * (P + 1) + r];
-            acc[mt] = cadd(acc[mt], cmul(pw, make_double2(fma(-Q, s_invr[r], d[mt][0]), d[mt][1])));
+            acc[mt] = cfma(pw, make_double2(fma(-Q, s_invr[r], d[mt][0]), d[mt][1]), acc[mt]);
           }
         }
       }
