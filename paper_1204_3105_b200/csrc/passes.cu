@@ -502,35 +502,42 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
       }
     }
     __syncwarp();
+    {
+      // both column tiles (sources 0-3 and 4-7 of the batch) in one sweep over k: each A fragment
+      // is read from shared memory once for the two DMMAs
+      const bool two = nb > 4;
+      double d[2][MT][2];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      if (4 * nt >= nb) break;
-      double d[MT][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) d[mt][0] = d[mt][1] = 0.0;
-      // B[k][n]: k = 4 kt + lane % 4, column n = 8 nt + lane / 4 -> source 4 nt + lane / 8, re/im (lane / 4) & 1
-      const int bs = 4 * nt + (lane >> 3), bc = (lane >> 2) & 1;
+      for (int mt = 0; mt < MT; ++mt) d[0][mt][0] = d[0][mt][1] = d[1][mt][0] = d[1][mt][1] = 0.0;
+      const int bs = lane >> 3, bc = (lane >> 2) & 1;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
-        const double2 v = s_at[bs * P + 4 * kt + (lane & 3)];
-        const double bfr = bc ? v.y : v.x;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma884(d[mt][0], d[mt][1], s_afr[(mt * KT + kt) * 32 + lane], bfr);
-      }
-      // C[r][2c + {0,1}] at lane 4r + c: row l = 8 mt + lane / 4 + R0, source s = 4 nt + lane % 4 (re, im)
-      const int s = 4 * nt + (lane & 3);
-      if (s < nb) {
-        const double Q = s_q[s];
+        const double2 v0 = s_at[bs * P + 4 * kt + (lane & 3)];
+        const double2 v1 = two ? s_at[(4 + bs) * P + 4 * kt + (lane & 3)] : make_double2(0.0, 0.0);
+        const double b0f = bc ? v0.y : v0.x, b1f = bc ? v1.y : v1.x;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const int r = 8 * mt + (lane >> 2) + R0;
-          if (r > P) continue;
-          if (!ROW0 && r == 0) {  // Y[0][s] (w^0 = 1; Q_s Log is in b0)
-            acc[mt].x += d[mt][0];
-            acc[mt].y += d[mt][1];
-          } else {
-            const double2 pw = s_pw[s * (P + 1) + r];
-            acc[mt] = cfma(pw, make_double2(fma(-Q, s_invr[r], d[mt][0]), d[mt][1]), acc[mt]);
+          const double a = s_afr[(mt * KT + kt) * 32 + lane];
+          dmma884(d[0][mt][0], d[0][mt][1], a, b0f);
+          if (two) dmma884(d[1][mt][0], d[1][mt][1], a, b1f);
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int s = 4 * nt + (lane & 3);
+        if (s < nb) {
+          const double Q = s_q[s];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int r = 8 * mt + (lane >> 2) + R0;
+            if (r > P) continue;
+            if (!ROW0 && r == 0) {
+              acc[mt].x += d[nt][mt][0];
+              acc[mt].y += d[nt][mt][1];
+            } else {
+              const double2 pw = s_pw[s * (P + 1) + r];
+              acc[mt] = cfma(pw, make_double2(fma(-Q, s_invr[r], d[nt][mt][0]), d[nt][mt][1]), acc[mt]);
+            }
           }
         }
       }
