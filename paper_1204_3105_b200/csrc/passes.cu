@@ -355,7 +355,10 @@ struct DownSmem {
   static constexpr int NB = 8, MT = ROW0 ? P / 8 : (P + 8) / 8, KT = P / 4;  // rows R0 .. R0 + 8 MT - 1
   static constexpr int afr_n = MT * KT * 32 + 8 * MT + 8;  // A fragments + 1/r table, r = 0..8 MT (+ padding)
   static constexpr size_t afr = sizeof(double) * afr_n;
-  static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * P + 32) + sizeof(double) * NB +
+  // a~ is stored as separate real and imaginary rows of PS doubles per source (the B fragment of a
+  // lane is one double); PS = 4 or 12 mod 16 keeps the 8 rows a fragment load touches on distinct banks
+  static constexpr int PS = (P % 16 == 4 || P % 16 == 12) ? P : P + 4;
+  static constexpr size_t warp = sizeof(double2) * (NB * (P + 1) + NB * PS + 32) + sizeof(double) * NB +
                                  sizeof(int) * FMM_CAND_MAX;
   static constexpr size_t bytes = afr + 4 * warp;
 };
@@ -379,15 +382,15 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
                                                      const double* __restrict__ binom, const double* __restrict__ tabs,
                                                      const double* __restrict__ afr, double2* __restrict__ loc_l) {
   using S = DownSmem<P>;
-  constexpr int NB = S::NB, MT = S::MT, KT = S::KT, R0 = S::R0;
+  constexpr int NB = S::NB, MT = S::MT, KT = S::KT, R0 = S::R0, PS = S::PS;
   constexpr bool ROW0 = S::ROW0;
   extern __shared__ double2 dsm[];
   double* s_afr = (double*)dsm;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char* wb = (char*)dsm + S::afr + w * S::warp;
   double2* s_pw = (double2*)wb;          // [NB][P+1] w_s^k
-  double2* s_at = s_pw + NB * (P + 1);   // [NB][P]   a~_{s,k}, k = 1..P
-  double2* s_b = s_at + NB * P;          // [32]      L2L part
+  double* s_at = (double*)(s_pw + NB * (P + 1));  // [NB][2][PS] Re / Im rows of a~_{s,k}, k = 1..P
+  double2* s_b = (double2*)(s_at + 2 * NB * PS);  // [32]      L2L part
   double* s_q = (double*)(s_b + 32);     // [NB]
   int* s_src = (int*)(s_q + NB);         // [FMM_CAND_MAX] E4(t)
   // the cell's own loads (everything that depends on t alone: target counts, E4 mask, centres, the
@@ -484,7 +487,8 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
           if (k <= P) s_pw[s * (P + 1) + k] = pw;
           if (k >= 1 && k <= P) {
             const double2 at = cmul(av[m], pw);  // (-1)^k is in Cb
-            s_at[s * P + k - 1] = at;
+            s_at[(2 * s) * PS + k - 1] = at.x;
+            s_at[(2 * s + 1) * PS + k - 1] = at.y;
             if (ROW0) y0 = cadd(y0, at);
           }
           pw = cmul(pw, w4);
@@ -512,9 +516,8 @@ __global__ void __launch_bounds__(128, DOWN_MINB(P)) k_down_mma(int l, int B, in
       const int bs = lane >> 3, bc = (lane >> 2) & 1;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
-        const double2 v0 = s_at[bs * P + 4 * kt + (lane & 3)];
-        const double2 v1 = two ? s_at[(4 + bs) * P + 4 * kt + (lane & 3)] : make_double2(0.0, 0.0);
-        const double b0f = bc ? v0.y : v0.x, b1f = bc ? v1.y : v1.x;
+        const double b0f = s_at[(2 * bs + bc) * PS + 4 * kt + (lane & 3)];
+        const double b1f = two ? s_at[(2 * (4 + bs) + bc) * PS + 4 * kt + (lane & 3)] : 0.0;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const double a = s_afr[(mt * KT + kt) * 32 + lane];
