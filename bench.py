@@ -64,7 +64,7 @@ F_PAIR = 45.0
 # {dfma,dadd,dmul}_pred_on; profiles/r02/fp64_counts.json), for the executed-rate line
 F_EXEC = {"C4q": 27.01, "C4s": 25.14, "C4t": 26.79, "C3": 44.48, "C5": 23.91}
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_p2p_pairs launch (ncu, profiles/r02/
-# launch_dram_table_<cfg>_r02f.txt); C4 = mean over its three launches.  The self-mode writes are
+# launch_dram_table_<cfg>_r02h.txt); C4 = mean over its three launches.  The self-mode writes are
 # the per-(target, near slot) partial sums (m x nslot x 16 B, less the paired tasks' unwritten
 # slots) that k_p2p_finish adds, the reads mostly the fills of their half-written 32-byte
 # sectors; distinct targets (C3) write one slot per target.
