@@ -273,17 +273,28 @@ def run_gpu(args):
         """serial: one stream; step: one stream per tiling forked and joined every step, so one
         tiling's copies overlap another tiling's kernels inside the step; cross: the streams
         alternate by step and join only at the end (copies also overlap the previous step)"""
-        one_step(host=True, pipelined=mode != "serial")
+        for _ in range(max(2, min(args.warmup, 3))):  # warm-up: every stream's pool blocks and pinned pages
+            one_step(host=True, pipelined=mode != "serial")
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = []
         f0.record(stream)
         for s_ in range(args.steps):
             if mode == "cross":  # a tiling's next copy waits only for its own previous step
                 one_step(host=True, pipelined=True, fork=(s_ < 2), join=(s_ >= args.steps - 2), parity=s_ % 2)
             else:
                 one_step(host=True, pipelined=mode == "step")
+            if mode != "cross":  # per-step marks (diagnostic only: the reported time is f0 -> f1)
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record(stream)
         f1.record(stream)
         barrier()
+        if marks and rank == 0:
+            prev, per = f0, []
+            for m_ in marks:
+                per.append(round(prev.elapsed_time(m_), 2))
+                prev = m_
+            log(f"[bench] e2e per-step ms ({mode}): {per}")
         t_ = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t_, op=dist.ReduceOp.MAX)
