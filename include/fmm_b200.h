@@ -127,7 +127,7 @@ typedef struct fmm_tree_s* fmm_tree_t;
  * Memory: the tree is one slab of the library's stream-ordered pool (fmm_tree_bytes; about
  * 0.65 KB per point in self mode at p = 24); during the build the sort takes scratch from the
  * same pool and returns it stream-ordered -- the bucket sort (K + 1) x 8 KB of leaf bins per
- * point set (it is only taken when that is <= 4 GB), the LSD sort 2 x 32 B per point.
+ * point set (it is only taken when that is <= 4 GB), the LSD sort about 40 B per point.
  * On success *out owns all device buffers until fmm_free. */
 int fmm_build_tree(const fmm_config* cfg, const double* src_xy, const double* src_u, int64_t n,
                    const double* tgt_xy, int64_t m, void* stream, fmm_tree_t* out);
